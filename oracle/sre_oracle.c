@@ -1,0 +1,274 @@
+/*
+ * sre_oracle.c -- TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain, slow, obviously-correct CPU oracle for the stabilizer Renyi entropy (SRE) of an
+ * N-qubit pure state, written from the paper (Sierant, Valles-Muns, Garcia-Saez,
+ * "Computing quantum magic of state vectors", arXiv:2601.07824; /root/reference/PAPER.md,
+ * cited below as P:<line>).
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference leg may
+ * load this library.  It shares no code, header, table or helper with the CUDA product path
+ * (paper_2601_07824_b200/csrc); neither includes the other.
+ *
+ * Three independent evaluations of the same sums, from three readings of the paper:
+ *   oracle_brute : Eq. (2) literally -- every <psi|X_a Z_b|psi> by applying Z_b, then X_a,
+ *                  to the state vector and taking the overlap.  O(8^N).
+ *   oracle_pauli : Eq. (2) over explicit tensor products of the 2x2 matrices I, X, Y, Z
+ *                  (no (a,b) parametrisation at all).  O(N 8^N).
+ *   oracle_fwht  : Alg. 2 literally -- for each X-string a: beta = X_a psi, v_x = conj(beta_x) alpha_x,
+ *                  complex in-place fast Hadamard transform (Eq. (13)), accumulate |chi_b|^{2q}.
+ *                  O(N 4^N).                                                    (Alg. 2)
+ *
+ * Sums layout (all three, and the finaliser):  sums[0..n_alpha-1] = S_{alpha_i} = sum_P t^{alpha_i}
+ * with t = |<P>|^2 (reading C2 of DESIGN.md: |chi|^{2q}, as SPEC's design decision),
+ * sums[n_alpha] = S_1 = sum_P t (purity, Eq. (14), lost_norm P:1162),
+ * sums[n_alpha+1] = sum_P t ln t  (for M_1, the q->1 limit of Eq. (2); 0 ln 0 = 0).
+ *
+ * Arithmetic: amplitudes are read as double, every product/sum is carried in long double
+ * (x87 80-bit), per-X-string sums are combined in ascending a order (deterministic for any
+ * thread count).  Integer alpha is raised by repeated multiplication, others by powl.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+typedef long double R;
+typedef struct { R re, im; } C;
+
+static int oracle_is_int(double a) { return a == floor(a) && a >= 1.0 && a <= 64.0; }
+
+/* t^alpha for t >= 0 (t = |<P>|^2). */
+static R oracle_pow(R t, double alpha) {
+  if (oracle_is_int(alpha)) {
+    R r = 1.0L;
+    for (int k = 0; k < (int)alpha; k++) r *= t;
+    return r;
+  }
+  if (t == 0.0L) return 0.0L;
+  return powl(t, (R)alpha);
+}
+
+/* Add the contribution of one expectation value with |<P>|^2 = t to a sums vector. */
+static void oracle_accumulate(R* acc, R t, const double* alpha, int n_alpha) {
+  for (int i = 0; i < n_alpha; i++) acc[i] += oracle_pow(t, alpha[i]);
+  acc[n_alpha] += t;
+  if (t > 0.0L) acc[n_alpha + 1] += t * logl(t);
+}
+
+static int popcount64(uint64_t v) { int c = 0; while (v) { c += (int)(v & 1u); v >>= 1; } return c; }
+
+/* ---------------------------------------------------------------------------------------------
+ * brute: <psi|P_{a,b}|psi> with P_{a,b} = X_a Z_b (Eq. (1)), applied as operators:
+ *   (Z_b psi)_x = (-1)^{b.x} psi_x        (Z_b|x> = (-1)^{b.x}|x>)
+ *   (X_a phi)_{x xor a} = phi_x           (X_a|x> = |x xor a>)
+ *   <psi|X_a Z_b psi> = sum_y conj(psi_y) (X_a Z_b psi)_y
+ * psi is interleaved (re, im) doubles of length 2*2^N.  If per_a != NULL it receives, for each
+ * a in [a_lo, a_hi), the (n_alpha + 2) sums restricted to that X-string.
+ * ------------------------------------------------------------------------------------------- */
+int oracle_brute(const double* psi, int N, const double* alpha, int n_alpha,
+                 uint64_t a_lo, uint64_t a_hi, double* sums, double* per_a) {
+  if (N < 1 || N > 14 || n_alpha < 1 || a_lo > a_hi) return 1;
+  const uint64_t D = (uint64_t)1 << N;
+  if (a_hi > D) return 1;
+  const int m = n_alpha + 2;
+  const uint64_t na = a_hi - a_lo;
+  R* pa = (R*)calloc((size_t)(na ? na : 1) * m, sizeof(R));
+  if (!pa) return 2;
+#pragma omp parallel
+  {
+    C* phi = (C*)malloc(sizeof(C) * D);
+    C* chi = (C*)malloc(sizeof(C) * D);
+#pragma omp for schedule(dynamic, 1)
+    for (int64_t k = 0; k < (int64_t)na; k++) {
+      uint64_t a = a_lo + (uint64_t)k;
+      R* acc = pa + (size_t)k * m;
+      for (uint64_t b = 0; b < D; b++) {
+        for (uint64_t x = 0; x < D; x++) {              /* phi = Z_b psi */
+          R s = (popcount64(b & x) & 1) ? -1.0L : 1.0L;
+          phi[x].re = s * psi[2 * x];
+          phi[x].im = s * psi[2 * x + 1];
+        }
+        for (uint64_t x = 0; x < D; x++) chi[x ^ a] = phi[x];  /* chi = X_a phi */
+        C e = {0.0L, 0.0L};
+        for (uint64_t y = 0; y < D; y++) {                /* <psi|chi> */
+          R pr = psi[2 * y], pi = psi[2 * y + 1];
+          e.re += pr * chi[y].re + pi * chi[y].im;
+          e.im += pr * chi[y].im - pi * chi[y].re;
+        }
+        oracle_accumulate(acc, e.re * e.re + e.im * e.im, alpha, n_alpha);
+      }
+    }
+    free(phi);
+    free(chi);
+  }
+  R* tot = (R*)calloc(m, sizeof(R));
+  for (uint64_t k = 0; k < na; k++)
+    for (int i = 0; i < m; i++) {
+      tot[i] += pa[k * m + i];
+      if (per_a) per_a[k * m + i] = (double)pa[k * m + i];
+    }
+  for (int i = 0; i < m; i++) sums[i] = (double)tot[i];
+  free(tot);
+  free(pa);
+  return 0;
+}
+
+/* ---------------------------------------------------------------------------------------------
+ * pauli: Eq. (2) summed over P = P_1 (x) ... (x) P_N with P_j in {I, X, Y, Z}, each
+ * applied as its explicit 2x2 matrix to qubit j (qubit j <-> bit j of the basis index):
+ *   I = [[1,0],[0,1]]  X = [[0,1],[1,0]]  Y = [[0,-i],[i,0]]  Z = [[1,0],[0,-1]].
+ * <psi|P|psi> is real for Hermitian P; the largest |Im| seen is returned in *max_imag.
+ * ------------------------------------------------------------------------------------------- */
+int oracle_pauli(const double* psi, int N, const double* alpha, int n_alpha, double* sums,
+                 double* max_imag) {
+  if (N < 1 || N > 8 || n_alpha < 1) return 1;
+  const uint64_t D = (uint64_t)1 << N;
+  uint64_t nP = 1;
+  for (int j = 0; j < N; j++) nP *= 4;
+  const int m = n_alpha + 2;
+  /* The four matrices, M[p][row][col] as complex. */
+  static const double Mre[4][2][2] = {{{1, 0}, {0, 1}}, {{0, 1}, {1, 0}}, {{0, 0}, {0, 0}}, {{1, 0}, {0, -1}}};
+  static const double Mim[4][2][2] = {{{0, 0}, {0, 0}}, {{0, 0}, {0, 0}}, {{0, -1}, {1, 0}}, {{0, 0}, {0, 0}}};
+  R* pp = (R*)calloc((size_t)nP * m, sizeof(R));
+  R* pim = (R*)calloc((size_t)nP, sizeof(R));
+#pragma omp parallel
+  {
+    C* cur = (C*)malloc(sizeof(C) * D);
+    C* nxt = (C*)malloc(sizeof(C) * D);
+#pragma omp for schedule(dynamic, 4)
+    for (int64_t code = 0; code < (int64_t)nP; code++) {
+      for (uint64_t x = 0; x < D; x++) { cur[x].re = psi[2 * x]; cur[x].im = psi[2 * x + 1]; }
+      uint64_t c = (uint64_t)code;
+      for (int j = 0; j < N; j++) {
+        int p = (int)(c & 3u);
+        c >>= 2;
+        for (uint64_t x = 0; x < D; x++) {              /* nxt = (1 (x) .. M_p on qubit j .. (x) 1) cur */
+          int row = (int)((x >> j) & 1u);
+          uint64_t x0 = x & ~((uint64_t)1 << j), x1 = x0 | ((uint64_t)1 << j);
+          R a_re = Mre[p][row][0], a_im = Mim[p][row][0];
+          R b_re = Mre[p][row][1], b_im = Mim[p][row][1];
+          nxt[x].re = a_re * cur[x0].re - a_im * cur[x0].im + b_re * cur[x1].re - b_im * cur[x1].im;
+          nxt[x].im = a_re * cur[x0].im + a_im * cur[x0].re + b_re * cur[x1].im + b_im * cur[x1].re;
+        }
+        C* t = cur; cur = nxt; nxt = t;
+      }
+      C e = {0.0L, 0.0L};
+      for (uint64_t y = 0; y < D; y++) {                  /* <psi|P psi> */
+        R pr = psi[2 * y], pi = psi[2 * y + 1];
+        e.re += pr * cur[y].re + pi * cur[y].im;
+        e.im += pr * cur[y].im - pi * cur[y].re;
+      }
+      oracle_accumulate(pp + (size_t)code * m, e.re * e.re, alpha, n_alpha);
+      pim[code] = fabsl(e.im);
+    }
+    free(cur);
+    free(nxt);
+  }
+  R tot[18] = {0};
+  R mi = 0.0L;
+  for (uint64_t k = 0; k < nP; k++) {
+    for (int i = 0; i < m; i++) tot[i] += pp[k * m + i];
+    if (pim[k] > mi) mi = pim[k];
+  }
+  for (int i = 0; i < m; i++) sums[i] = (double)tot[i];
+  if (max_imag) *max_imag = (double)mi;
+  free(pp);
+  free(pim);
+  return 0;
+}
+
+/* ---------------------------------------------------------------------------------------------
+ * fwht: Algorithm 2.  For each X-string a in [a_lo, a_hi):
+ *   beta_x = (X_a psi)_x = psi_{x xor a}            (line 3, |psi'> = X_a |psi>)
+ *   v_x = conj(beta_x) * alpha_x, alpha_x = psi_x    (line 4, Eq. (12))
+ *   chi = H_2^{(x)N} v, unnormalised H_2 = [[1,1],[1,-1]], in place (line 5, Eq. (13))
+ *   S_q += sum_b |chi_b|^{2q}                        (line 6, modulus reading C2)
+ * The Gray-code stepping of lines 7-8 only changes the order in which a is visited (reading C11).
+ * per_a (optional) receives the (n_alpha+2) sums of each X-string; chi_out (optional, only when
+ * a_hi - a_lo == 1) receives the complex chi_b, b = 0 .. 2^N-1, interleaved as doubles.
+ * ------------------------------------------------------------------------------------------- */
+int oracle_fwht(const double* psi, int N, const double* alpha, int n_alpha,
+                uint64_t a_lo, uint64_t a_hi, double* sums, double* per_a, double* chi_out) {
+  if (N < 1 || N > 26 || n_alpha < 1 || n_alpha > 16 || a_lo > a_hi) return 1;
+  const uint64_t D = (uint64_t)1 << N;
+  if (a_hi > D) return 1;
+  const int m = n_alpha + 2;
+  const uint64_t na = a_hi - a_lo;
+  R* pa = (R*)calloc((size_t)(na ? na : 1) * m, sizeof(R));
+  if (!pa) return 2;
+  int err = 0;
+#pragma omp parallel
+  {
+    C* v = (C*)malloc(sizeof(C) * D);
+    if (!v) {
+#pragma omp atomic write
+      err = 2;
+    }
+#pragma omp for schedule(dynamic, 1)
+    for (int64_t k = 0; k < (int64_t)na; k++) {
+      if (!v) continue;
+      uint64_t a = a_lo + (uint64_t)k;
+      for (uint64_t x = 0; x < D; x++) {
+        R br = psi[2 * (x ^ a)], bi = psi[2 * (x ^ a) + 1];   /* beta_x */
+        R ar = psi[2 * x], ai = psi[2 * x + 1];               /* alpha_x */
+        v[x].re = br * ar + bi * ai;                          /* conj(beta) * alpha */
+        v[x].im = br * ai - bi * ar;
+      }
+      for (uint64_t h = 1; h < D; h <<= 1)                    /* fast Hadamard transform */
+        for (uint64_t i = 0; i < D; i += 2 * h)
+          for (uint64_t j = i; j < i + h; j++) {
+            C u = v[j], w = v[j + h];
+            v[j].re = u.re + w.re; v[j].im = u.im + w.im;
+            v[j + h].re = u.re - w.re; v[j + h].im = u.im - w.im;
+          }
+      R* acc = pa + (size_t)k * m;
+      for (uint64_t b = 0; b < D; b++) oracle_accumulate(acc, v[b].re * v[b].re + v[b].im * v[b].im, alpha, n_alpha);
+      if (chi_out && na == 1)
+        for (uint64_t b = 0; b < D; b++) { chi_out[2 * b] = (double)v[b].re; chi_out[2 * b + 1] = (double)v[b].im; }
+    }
+    free(v);
+  }
+  if (!err) {
+    R* tot = (R*)calloc(m, sizeof(R));
+    for (uint64_t k = 0; k < na; k++)
+      for (int i = 0; i < m; i++) {
+        tot[i] += pa[k * m + i];
+        if (per_a) per_a[k * m + i] = (double)pa[k * m + i];
+      }
+    for (int i = 0; i < m; i++) sums[i] = (double)tot[i];
+    free(tot);
+  }
+  free(pa);
+  return err;
+}
+
+/* ---------------------------------------------------------------------------------------------
+ * finalize: Eq. (2) from the sums.
+ *   alpha != 1 : M = log2(S_alpha / 2^N) / (1 - alpha)
+ *   alpha == 1 : M_1 = -2^{-N} sum_P t log2 t     (q -> 1 limit, reading C4)
+ *   lost_norm  = 1 - S_1 / 2^N
+ * ------------------------------------------------------------------------------------------- */
+int oracle_finalize(const double* sums, int N, const double* alpha, int n_alpha, double* M,
+                    double* lost_norm) {
+  const double D = ldexp(1.0, N);
+  for (int i = 0; i < n_alpha; i++) {
+    if (alpha[i] == 1.0)
+      M[i] = -(sums[n_alpha + 1] / log(2.0)) / D;
+    else
+      M[i] = log2(sums[i] / D) / (1.0 - alpha[i]);
+  }
+  if (lost_norm) *lost_norm = 1.0 - sums[n_alpha] / D;
+  return 0;
+}
+
+int oracle_num_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
