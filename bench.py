@@ -1,0 +1,319 @@
+#!/usr/bin/env python
+"""Benchmark of the exact-SRE hot path (BASELINE.json metric: exact SRE M_2 Pauli strings/s).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4|c2|c3|c5] [--impl reference]
+
+A step = one full evaluation of Alg. 2 for the config's workload: every
+X-string's generation + Walsh-Hadamard transform + FP64 power sums, the reduction, the
+cross-GPU allreduce (N > 1) and the host finalisation of Eq. (2).  Default workload: BASELINE
+config 4 (N = 20 seeded Haar state, alpha = 2), 4^20 Pauli strings per step.  Under torchrun the
+2^N X-strings are split into contiguous equal shards, one per rank, and the (n_alpha + 2) partial
+sums are combined with one NCCL all_reduce per step (strong scaling: total work fixed).
+
+``--impl reference`` times the CPU oracle (oracle/, plain C, long double) on the host cores on a
+bounded sample of the same workload (the only reference this paper-only task has).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "exact SRE M_2 Pauli strings/s at N=20/24 on 1-8 B200; FWHT HBM GB/s vs peak"
+CONFIGS = {
+    # name: (workload label, N, batch, alphas, seed)
+    "c4": ("N=20 seeded Haar state, alpha=2 (BASELINE config 4)", 20, 1, [2.0], 20001),
+    "c2": ("N=16 seeded Haar state, alpha in {1,2,3} (BASELINE config 2)", 16, 1, [1.0, 2.0, 3.0], 16001),
+    "c3": ("256 x N=14 Clifford+T states, alpha=2 (BASELINE config 3)", 14, 256, [2.0], 14000),
+    "c5": ("N=24 seeded Haar state, alpha=2 (BASELINE config 5)", 24, 1, [2.0], 24001),
+}
+FP64_OPS_PER_CLK_SM = 64        # B200 FP64 pipe (measured 63.9/clk/SM, profiles/r01_microbench.json)
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def make_state(cfg):
+    import sre_inputs as si
+    _, n, b, _, seed = CONFIGS[cfg]
+    if cfg == "c3":
+        batch, _ = si.config3_batch(n, b, seed)
+        return batch
+    return si.haar(n, seed)
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (the recipe's clocks line)."""
+
+    def __init__(self, gpu_index):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={gpu_index}", f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows]
+        mx = float(rows[0][2])
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].strip().lower() == "active"})
+        loaded = [s for s in sm if s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(rows), "power_w_max": max(float(r[3]) for r in rows)}
+
+
+def cpu_sample(cfg, seconds_target=15.0):
+    """Oracle (Alg. 2, long double, OpenMP) on a bounded slice of the workload's X-strings."""
+    import oracle
+    label, n, b, alphas, seed = CONFIGS[cfg]
+    psi = make_state(cfg)
+    one = psi[0] if b > 1 else psi
+    # calibrate the slice: X-strings cost N 2^N each, uniform
+    threads = oracle.num_threads()
+    k = max(threads, 1)
+    t0 = time.perf_counter()
+    oracle.sums_fwht(one, alphas, a_range=(0, k))
+    dt = time.perf_counter() - t0
+    per_a = dt / k
+    k2 = int(min(1 << n, max(threads, seconds_target / max(per_a, 1e-9))))
+    k2 = max(threads, (k2 // threads) * threads)
+    t0 = time.perf_counter()
+    oracle.sums_fwht(one, alphas, a_range=(0, k2))
+    dt = time.perf_counter() - t0
+    paulis = k2 * float(1 << n)
+    return {"value": paulis / dt, "unit": "Pauli strings/s", "cores": threads, "kind": "oracle",
+            "sample": f"oracle fwht (Alg. 2, long double) over X-strings [0, {k2}) of the {label}; "
+                      f"{k2} x 2^{n} Pauli strings in {dt:.2f} s", "seconds": dt}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cfg = args.config
+    label, n, b, alphas, seed = CONFIGS[cfg]
+    import oracle
+    oracle.build()
+    psi = make_state(cfg)
+    one = psi[0] if b > 1 else psi
+    threads = oracle.num_threads()
+    # each step: a bounded slice sized so the whole run stays within a few minutes
+    k = max(threads, 1)
+    t0 = time.perf_counter()
+    oracle.sums_fwht(one, alphas, a_range=(0, k))
+    per_a = (time.perf_counter() - t0) / k
+    budget = 150.0 / max(1, args.steps + args.warmup)
+    ka = int(max(threads, min(1 << n, budget / max(per_a, 1e-9))))
+    ka = max(threads, (ka // threads) * threads)
+    for _ in range(args.warmup):
+        oracle.sums_fwht(one, alphas, a_range=(0, ka))
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.sums_fwht(one, alphas, a_range=(0, ka))
+        times.append(time.perf_counter() - t0)
+    dt = sum(times)
+    value = args.steps * ka * float(1 << n) / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "Pauli strings/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64 (long double accum)",
+        "data": "synthetic", "config": {"workload": label, "N": n, "batch": b, "alphas": alphas, "seed": seed,
+                                        "x_strings_per_step": ka},
+        "cpu_baseline": {"value": value, "unit": "Pauli strings/s", "cores": threads, "kind": "oracle",
+                         "sample": f"oracle fwht over X-strings [0, {ka}) per step ({ka} of 2^{n})"},
+        "e2e": {"value": value, "unit": "Pauli strings/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-stride", type=int, default=16)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2601_07824_b200 as sre
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    label, n, b, alphas, seed = CONFIGS[args.config]
+    D = 1 << n
+    lo, hi = rank * D // world, (rank + 1) * D // world   # contiguous X-string shard
+    psi_host = make_state(args.config)
+    psi = torch.from_numpy(psi_host).to(dev)            # replicated on every GPU (same seed)
+    ws = torch.empty(sre.workspace_size(n, b, len(alphas)), dtype=torch.uint8, device=dev)
+    sums = torch.empty((b, len(alphas) + 2), dtype=torch.float64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > L2 (126 MB)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        sre.partial_sums(psi, lo, hi, alphas, out=sums, workspace=ws, stream=stream)
+        if world > 1:
+            dist.all_reduce(sums)                        # the one exchange step (NCCL, NVLink)
+        return sre.finalize(sums, n, alphas)             # D2H of (n_alpha+2) doubles per state
+
+    for _ in range(max(args.warmup, 0)):
+        m, ln = step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = Clocks(local) if rank == 0 or True else None
+    launches0 = sre.launch_count()
+    sre.profile_begin(args.profile_stride)
+    step_ms = []
+    for _ in range(args.steps):
+        flush.fill_(1)                                   # L2 flush between timed steps (untimed)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        m, ln = step()
+        e1.record(stream)
+        e1.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+    prof = sre.profile_end()
+    launches = sre.launch_count() - launches0
+    torch.cuda.synchronize()
+    clk = clocks.stop() if clocks else None
+    tot_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+        dist.barrier()
+    paulis_per_step = float(b) * 4.0 ** n
+    value = args.steps * paulis_per_step / (tot_ms * 1e-3)
+
+    # ---- end-to-end through the public C entry with host (pinned) buffers, N=1 semantics per rank
+    e2e = None
+    if world == 1:
+        pinned = torch.from_numpy(psi_host).pin_memory()
+        fn = sre.exact if b == 1 else sre.exact_batched
+        fn(pinned, alphas)
+        torch.cuda.synchronize()
+        t_e = []
+        for _ in range(max(1, min(args.steps, 3))):
+            t0 = time.perf_counter()
+            fn(pinned, alphas)                             # H2D copy + norm check + sweep + D2H inside
+            t_e.append(time.perf_counter() - t0)
+        e2e = {"value": paulis_per_step * len(t_e) / sum(t_e), "unit": "Pauli strings/s",
+               "h2d_bytes_per_step": int(psi_host.nbytes), "d2h_bytes_per_step": int(8 * b * (len(alphas) + 2)),
+               "ms_per_step": 1e3 * sum(t_e) / len(t_e)}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    peaks, peak_src = load_peaks()
+    # dominant kernel and its roofline
+    kinds = {k: v for k, v in prof.items() if v["timed"] > 0 and k != "aux"}
+    share = {k: v["ms_sum"] / v["timed"] * v["launched"] for k, v in kinds.items()}
+    dom = max(share, key=share.get)
+    avg_ms = prof[dom]["ms_sum"] / prof[dom]["timed"]
+    launched = prof[dom]["launched"]
+    paulis_per_launch = paulis_per_step * args.steps / max(1, world) / launched
+    nq = n
+    # FP64 ops per Pauli string per kernel kind
+    ops = {"single_pass": 2 + (nq - 1) + 3, "pass_a": 2 + 0, "pass_b": 3}
+    if dom == "pass_a":
+        L = {15: 10, 16: 10, 17: 10, 18: 10, 19: 10, 20: 10, 21: 11, 22: 12, 23: 13}.get(nq, 13)
+        ops_unit = 2 + L
+        bytes_unit = 8 + 16.0 / 1.0   # workspace write + psi reads (two complex per 2 outputs)
+    elif dom == "pass_b":
+        L = {15: 10, 16: 10, 17: 10, 18: 10, 19: 10, 20: 10, 21: 11, 22: 12, 23: 13}.get(nq, 13)
+        ops_unit = (nq - 1 - L) + 3
+        bytes_unit = 8.0
+    else:
+        ops_unit = ops["single_pass"]
+        bytes_unit = 16.0
+    sm_mhz = (clk or {}).get("sm_max_mhz", peaks.get("sm_max_mhz", 1965.0))
+    if n >= 23:
+        peak = peaks["hbm_gbs"]
+        achieved = bytes_unit * paulis_per_launch / (avg_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": None, "peak_source": peak_src}
+    else:
+        peak = FP64_OPS_PER_CLK_SM * 148 * sm_mhz * 1e6 / 1e12
+        achieved = ops_unit * paulis_per_launch / (avg_ms * 1e-3) / 1e12
+        roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s (FP64 ops)",
+                "frac": achieved / peak, "traffic": None,
+                "peak_source": f"64 FP64 ops/clk/SM x 148 SMs x {sm_mhz:.0f} MHz (guide unit count; measured 63.9)"}
+    roof.update({"kernel": dom, "avg_launch_ms": avg_ms, "launches_timed": prof[dom]["timed"],
+                 "share_of_step": share[dom] / tot_ms if world == 1 else None,
+                 "ops_per_pauli": ops_unit, "bytes_per_pauli": bytes_unit})
+    hbm_equiv = 16.0 * value / max(1, world) / 1e9      # FWHT workspace bytes per Pauli string (16 B)
+    line = {
+        "metric": METRIC, "value": value, "unit": "Pauli strings/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": label, "N": n, "batch": b, "alphas": alphas, "seed": seed,
+                   "x_string_shards": world, "l2": "flushed between steps (256 MiB write)",
+                   "step": "partial_sums over all 2^N X-strings + allreduce + finalize"},
+        "roofline": roof,
+        "fwht_hbm_equiv": {"GBps_per_gpu": hbm_equiv, "frac_of_hbm": hbm_equiv / peaks["hbm_gbs"],
+                           "note": "16 B/Pauli string workspace write+read, vs measured HBM copy bandwidth"},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+        "e2e": e2e,
+        "result": {"M": [float(x) for x in m[0]], "lost_norm": float(ln[0])},
+        "profile": prof,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        import oracle
+        oracle.build()
+        line["cpu_baseline"] = cpu_sample(args.config)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,141 @@
+/*
+ * sre.h -- C ABI of libsre_b200.so: exact stabilizer Renyi entropy of N-qubit pure states on
+ * NVIDIA B200 (sm_100a).
+ *
+ * Operation (PAPER.md = Sierant, Valles-Muns, Garcia-Saez, arXiv:2601.07824):
+ *   M_alpha(|psi>) = 1/(1-alpha) log2[ sum_{a,b in Z_2^N} |<psi|X_a Z_b|psi>|^{2 alpha} / 2^N ]
+ *       -- Eq. (2), with the modulus reading of chi^{2q} (reading C2);
+ *   M_1 = -2^{-N} sum_P t log2 t, t = |<P>|^2  -- the alpha -> 1 limit (reading C4);
+ *   lost_norm = 1 - sum_P <P>^2 / 2^N          -- P:1162.
+ * computed by Algorithm 2: for every X-string a, chi_b(a) = sum_x conj(psi_{x^a}) psi_x
+ * (-1)^{b.x} (Eq. (12)) for all b at once by a fast Walsh-Hadamard transform (Eq. (13)), and the
+ * power sums of Eq. (11) accumulated in FP64.  The GPU kernels use the exact half-length
+ * complex reformulation described in DESIGN.md ("Half-length transform").
+ *
+ * Conventions for every entry point:
+ *   - psi: complex128 amplitudes, interleaved (re, im) doubles, index x = sum_j x_j 2^j (qubit j
+ *     is bit j).  Batched calls take B contiguous states [B][2^N].  16-byte aligned.
+ *   - Pointers are plain host or device addresses on the current CUDA device; no ownership is
+ *     transferred; the library never frees caller memory.
+ *   - Every function returns an int status (sre_status) and never aborts; on error the output
+ *     buffers are left untouched and sre_last_error() holds a one-line reason.
+ *   - Supported sizes: 1 <= N <= 26, 1 <= n_alpha <= 16, every alpha finite and > 0
+ *     (alpha == 1 exactly selects the Shannon branch; reading C5).
+ */
+#ifndef SRE_B200_H
+#define SRE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SRE_OK = 0,
+  SRE_EINVAL = 1,      /* bad argument: null pointer, n_alpha out of range, alpha <= 0 / NaN */
+  SRE_ERANGE = 2,      /* N outside [1, 26], B < 1, or a_begin/a_end outside [0, 2^N] */
+  SRE_ENOTNORM = 3,    /* | ||psi||^2 - 1 | > 1e-8 (reading C6; checked by the synchronous calls) */
+  SRE_EWORKSPACE = 4,  /* caller workspace smaller than sre_workspace_size() */
+  SRE_ENOMEM = 5,      /* device allocation failed */
+  SRE_ECUDA = 6,       /* CUDA runtime / launch error (text in sre_last_error) */
+  SRE_EINTERNAL = 7,   /* internal consistency check failed */
+  SRE_ENODEV = 8       /* no sm_100 device visible */
+} sre_status;
+
+#define SRE_MAX_N 26
+#define SRE_MAX_ALPHA 16
+
+/* Static string for a status code. */
+const char* sre_status_string(int code);
+/* Thread-local detail of the last error (empty string if none). */
+const char* sre_last_error(void);
+/* ABI version (major*100 + minor). */
+int sre_version(void);
+
+/*
+ * sre_exact -- M_alpha for one state, synchronous (Alg. 2 over all 2^N X-strings).
+ *   psi      : host OR device pointer to 2^N complex128 (a host pointer is copied to the device
+ *              inside the call: this is the end-to-end path).
+ *   alpha    : host array [n_alpha] of Renyi indices.
+ *   out_M    : host array [n_alpha], M_alpha in bits.
+ *   out_lost_norm : host pointer to one double (nullable), lost_norm of P:1162.
+ * Uses the legacy default stream and an internally cached workspace.
+ */
+int sre_exact(const void* psi, int N, const double* alpha, int n_alpha, double* out_M,
+              double* out_lost_norm);
+
+/*
+ * sre_exact_batched -- B independent states psi[B][2^N] (BASELINE config 3).
+ *   out_M : host [B][n_alpha] row-major; out_lost_norm : host [B] (nullable).
+ */
+int sre_exact_batched(const void* psi, int N, int B, const double* alpha, int n_alpha,
+                      double* out_M, double* out_lost_norm);
+
+/*
+ * sre_workspace_size -- bytes of device workspace sre_partial_sums needs for (N, B, n_alpha).
+ * Returns 0 for unsupported arguments.
+ */
+size_t sre_workspace_size(int N, int B, int n_alpha);
+
+/*
+ * sre_partial_sums -- asynchronous building block (multi-GPU sharding, checkpointed ranges).
+ * Accumulates, for every state and for the X-strings a in [a_begin, a_end) only
+ * (the chunked loop of P:314 / P:1179-1183), the raw sums of Eq. (11):
+ *   sums_dev[s*(n_alpha+2) + i]         = sum_{a in range, b} t^{alpha_i}   (i < n_alpha)
+ *   sums_dev[s*(n_alpha+2) + n_alpha]   = sum_{a in range, b} t             (purity, Eq. (14))
+ *   sums_dev[s*(n_alpha+2) + n_alpha+1] = sum_{a in range, b} t ln t        (0 ln 0 = 0)
+ * with t = |<psi|X_a Z_b|psi>|^2.  sums_dev is overwritten (device memory, [B][n_alpha+2]).
+ * Sums over disjoint ranges add; they are deterministic for a given (range, N, B).
+ *   psi       : device pointer, [B][2^N] complex128.
+ *   alpha     : host array [n_alpha] (copied).
+ *   workspace : device buffer of ws_bytes >= sre_workspace_size(N, B, n_alpha).
+ *   stream    : cudaStream_t (NULL = legacy default stream); all work is enqueued on it.
+ * No norm check (the caller owns it); a_begin == a_end writes zeros.
+ */
+int sre_partial_sums(const void* psi, int N, int B, uint64_t a_begin, uint64_t a_end,
+                     const double* alpha, int n_alpha, void* workspace, size_t ws_bytes,
+                     double* sums_dev, void* stream);
+
+/*
+ * sre_finalize -- host-side Eq. (2) from complete sums (all 2^N X-strings):
+ *   alpha != 1: M = log2(S_alpha / 2^N) / (1 - alpha);  alpha == 1: M = -(sum t ln t)/(2^N ln 2);
+ *   lost_norm = 1 - S_1 / 2^N.
+ *   sums_host: [B][n_alpha+2] as produced by sre_partial_sums; out_M [B][n_alpha];
+ *   out_lost_norm [B] (nullable).
+ */
+int sre_finalize(const double* sums_host, int N, int B, const double* alpha, int n_alpha,
+                 double* out_M, double* out_lost_norm);
+
+/*
+ * sre_norm2 -- ||psi_s||^2 for each of B device states into device out_dev[B] (FP64, async).
+ */
+int sre_norm2(const void* psi, int N, int B, double* out_dev, void* stream);
+
+/*
+ * sre_chi -- debug/verification entry: chi_b(a) = <psi|X_a Z_b|psi> for one X-string a and all
+ * b (Eq. (12)), computed by the same kernels as the sums, written to device chi_dev[2*2^N]
+ * as complex128 in natural b order (each chi is purely real or purely imaginary, DESIGN C3).
+ */
+int sre_chi(const void* psi, int N, uint64_t a, double* chi_dev, void* stream);
+
+/*
+ * Instrumentation used by bench.py (no effect on results).
+ *   sre_launch_count   : cumulative number of kernels this library launched in the process.
+ *   sre_profile_begin  : start sampling; every stride-th launch of each kernel kind is bracketed
+ *                        by CUDA events on its own stream.
+ *   sre_profile_end    : stop; per kind k (0 single-pass, 1 pass A, 2 pass B, 3 auxiliary)
+ *                        ms_sum[k] = summed event time of the sampled launches, n_timed[k] = how
+ *                        many were sampled, n_launched[k] = launches of that kind since begin.
+ *                        Arrays have 4 entries each (any may be NULL).  Synchronises the events.
+ */
+uint64_t sre_launch_count(void);
+int sre_profile_begin(int stride);
+int sre_profile_end(double* ms_sum, uint64_t* n_timed, uint64_t* n_launched);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SRE_B200_H */

@@ -1,0 +1,671 @@
+// sre_api.cu -- C ABI of libsre_b200.so (include/sre.h): validation, planning, workspace,
+// launch schedule and finalisation for the exact SRE hot path (Alg. 2).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <atomic>
+#include <mutex>
+#include <vector>
+
+#include "../../include/sre.h"
+#include "sre_kernels.cuh"
+
+using namespace sre;
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+#define CK(x)                                                                                 \
+  do {                                                                                        \
+    cudaError_t e_ = (x);                                                                     \
+    if (e_ != cudaSuccess) return fail(SRE_ECUDA, "%s: %s (%s:%d)", #x, cudaGetErrorString(e_), \
+                                       __FILE__, __LINE__);                                   \
+  } while (0)
+
+// ------------------------------------------------------------------------------------------
+// launch accounting and sampled per-kernel timing (bench.py's roofline numbers)
+// ------------------------------------------------------------------------------------------
+enum LaunchKind { LK_SINGLE = 0, LK_PASSA = 1, LK_PASSB = 2, LK_AUX = 3, LK_N = 4 };
+
+struct Prof {
+  std::mutex mu;
+  bool on = false;
+  int stride = 1;
+  uint64_t launched[LK_N] = {0, 0, 0, 0};
+  std::vector<cudaEvent_t> pool;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed[LK_N];
+};
+Prof g_prof;
+std::atomic<uint64_t> g_launches{0};
+
+cudaEvent_t prof_event() {
+  if (!g_prof.pool.empty()) {
+    cudaEvent_t e = g_prof.pool.back();
+    g_prof.pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Wraps one kernel launch: counts it, and when profiling, brackets every stride-th launch of
+// its kind with CUDA events on the launching stream.
+template <class F>
+cudaError_t launch_counted(int kind, cudaStream_t st, F&& f) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (!g_prof.on) return f();
+  std::lock_guard<std::mutex> lk(g_prof.mu);
+  const bool sample = (g_prof.launched[kind]++ % (uint64_t)g_prof.stride) == 0;
+  if (!sample) return f();
+  cudaEvent_t a = prof_event(), b = prof_event();
+  cudaEventRecord(a, st);
+  cudaError_t e = f();
+  cudaEventRecord(b, st);
+  g_prof.timed[kind].push_back({a, b});
+  return e;
+}
+
+struct Dev {
+  int id = -1, sms = 0, major = 0, minor = 0;
+};
+
+int get_dev(Dev& d) {
+  int id = 0;
+  cudaError_t e = cudaGetDevice(&id);
+  if (e != cudaSuccess) return fail(SRE_ENODEV, "cudaGetDevice: %s", cudaGetErrorString(e));
+  static std::mutex mu;
+  static Dev cache[64];
+  std::lock_guard<std::mutex> lk(mu);
+  if (id < 0 || id >= 64) return fail(SRE_ENODEV, "device id %d", id);
+  if (cache[id].id != id) {
+    cudaDeviceProp pr;
+    CK(cudaGetDeviceProperties(&pr, id));
+    if (pr.major != 10) return fail(SRE_ENODEV, "device %d is sm_%d%d; libsre_b200 is built for sm_100a", id, pr.major, pr.minor);
+    cache[id].id = id;
+    cache[id].sms = pr.multiProcessorCount;
+    cache[id].major = pr.major;
+    cache[id].minor = pr.minor;
+  }
+  d = cache[id];
+  return SRE_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// plan
+// ------------------------------------------------------------------------------------------
+enum Kind { SMALL = 0, MID = 1, TWOPASS = 2 };
+
+struct Plan {
+  int N = 0, T = 0, kind = 0;
+  int L = 0, H = 0, CB = 0, TP = 0, K = 0;  // two-pass
+  int unitsA = 0, unitsB = 0, blkB = 0;
+  size_t slab_doubles = 0;  // K * 2^N
+  size_t slots = 0;         // partial slots per state
+};
+
+void two_pass_params(int T, int& L, int& H, int& CB) {
+  L = T - 9;
+  if (L < 10) L = 10;
+  if (L > 13) L = 13;
+  H = T - L;
+  CB = 13 - H;
+  if (CB > 6) CB = 6;
+  if (CB < 2) CB = 2;
+}
+
+constexpr int SMALL_MAX_T = 10;
+constexpr int MID_MAX_T = 13;
+
+// CTAs per state for the single-pass kernels: minimise waves x per-CTA items (uniform cost).
+int pick_gx(uint64_t count, int per_cta, int B, int resident) {
+  uint64_t best = ~0ull;
+  int bg = 1;
+  const uint64_t maxg = (count + per_cta - 1) / per_cta;
+  for (int g = 1; g <= 4096 && (uint64_t)g <= maxg; ++g) {
+    const uint64_t waves = ((uint64_t)B * g + resident - 1) / resident;
+    const uint64_t items = (count + (uint64_t)g * per_cta - 1) / ((uint64_t)g * per_cta);
+    const uint64_t cost = waves * items;
+    if (cost < best) { best = cost; bg = g; }
+  }
+  return bg;
+}
+
+int make_plan(int N, const Dev& d, Plan& p) {
+  p.N = N;
+  p.T = N - 1;
+  if (p.T <= SMALL_MAX_T) {
+    p.kind = SMALL;
+    p.slots = 4096;
+  } else if (p.T <= MID_MAX_T) {
+    p.kind = MID;
+    p.slots = 4096;
+  } else {
+    p.kind = TWOPASS;
+    two_pass_params(p.T, p.L, p.H, p.CB);
+    p.TP = p.CB + p.H;
+    uint64_t k = (1ull << 23) >> N;  // K * 2^N doubles ~ 64 MiB of workspace in flight
+    if (k < 2) k = 2;
+    if (k > 64) k = 64;
+    p.K = (int)k;
+    p.unitsA = 256 >> (p.L - 5);
+    p.blkB = p.TP >= 14 ? 512 : 256;
+    p.unitsB = p.blkB >> (p.TP - 5);
+    p.slab_doubles = (size_t)p.K << N;
+    const uint64_t itemsB = (uint64_t)p.K * 2 * (1ull << (p.L - p.CB));
+    p.slots = (size_t)((itemsB + p.unitsB - 1) / p.unitsB);
+  }
+  (void)d;
+  return SRE_OK;
+}
+
+size_t ws_bytes_for(const Plan& p, int B) {
+  size_t partial = p.slots * NACC * (p.kind == TWOPASS ? 1 : (size_t)B);
+  size_t norm = 4096 * (size_t)B + (size_t)B;
+  return (partial + p.slab_doubles + norm) * sizeof(double) + 256;
+}
+
+// ------------------------------------------------------------------------------------------
+// alpha sweeps
+// ------------------------------------------------------------------------------------------
+struct Sweep {
+  Alphas al;
+  int first = 0;
+  bool a2 = false;
+  double scale4[MAXA];
+};
+
+std::vector<Sweep> make_sweeps(const double* alpha, int n_alpha) {
+  std::vector<Sweep> sw;
+  bool any_one = false;
+  for (int i = 0; i < n_alpha; ++i) any_one |= (alpha[i] == 1.0);
+  for (int f = 0; f < n_alpha; f += MAXA) {
+    Sweep s;
+    memset(&s.al, 0, sizeof(s.al));
+    s.first = f;
+    s.al.n = n_alpha - f < MAXA ? n_alpha - f : MAXA;
+    s.al.need_log = (f == 0 && any_one) ? 1 : 0;
+    for (int i = 0; i < s.al.n; ++i) {
+      const double a = alpha[f + i];
+      s.al.alpha[i] = a;
+      if (a == std::floor(a) && a >= 1.0 && a <= 64.0) {
+        s.al.kind[i] = 0;
+        s.al.iexp[i] = (int)a;
+      } else {
+        s.al.kind[i] = 2;
+        s.al.iexp[i] = 0;
+      }
+      s.scale4[i] = std::pow(4.0, a);  // t = 4 t'  =>  t^alpha = 4^alpha t'^alpha
+    }
+    s.a2 = (s.al.n == 1 && alpha[f] == 2.0 && !s.al.need_log);
+    sw.push_back(s);
+  }
+  return sw;
+}
+
+// ------------------------------------------------------------------------------------------
+// launchers (template dispatch)
+// ------------------------------------------------------------------------------------------
+template <int T, bool A2, bool DBG>
+cudaError_t launch_small_t(const double2* psi, int N, int B, int gx, uint64_t a0, uint64_t count, const Alphas& al,
+                           double* partial, double* chi, cudaStream_t st) {
+  dim3 grid(gx, B);
+  return launch_counted(LK_SINGLE, st, [&] {
+    k_small<T, A2, DBG><<<grid, 256, 0, st>>>(psi, N, a0, count, al, partial, chi);
+    return cudaGetLastError();
+  });
+}
+
+template <bool A2, bool DBG>
+cudaError_t launch_small(int T, const double2* psi, int N, int B, int gx, uint64_t a0, uint64_t count, const Alphas& al,
+                         double* partial, double* chi, cudaStream_t st) {
+  switch (T) {
+#define C_(t) case t: return launch_small_t<t, A2, DBG>(psi, N, B, gx, a0, count, al, partial, chi, st);
+    C_(0) C_(1) C_(2) C_(3) C_(4) C_(5) C_(6) C_(7) C_(8) C_(9) C_(10)
+#undef C_
+  }
+  return cudaErrorInvalidValue;
+}
+
+constexpr int SMEM_128K = 2 * 32 * 256 * 8;
+
+template <class K>
+cudaError_t set_smem(K kern, int bytes) {
+  return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+template <int T, bool A2, bool DBG>
+cudaError_t launch_mid_t(const double2* psi, int N, int B, int gx, uint64_t a0, uint64_t count, const Alphas& al,
+                         double* partial, double* chi, cudaStream_t st) {
+  static bool init = false;
+  if (!init) {
+    cudaError_t e = set_smem(k_mid<T, A2, DBG>, SMEM_128K);
+    if (e != cudaSuccess) return e;
+    init = true;
+  }
+  dim3 grid(gx, B);
+  return launch_counted(LK_SINGLE, st, [&] {
+    k_mid<T, A2, DBG><<<grid, 256, SMEM_128K, st>>>(psi, N, a0, count, al, partial, chi);
+    return cudaGetLastError();
+  });
+}
+
+template <bool A2, bool DBG>
+cudaError_t launch_mid(int T, const double2* psi, int N, int B, int gx, uint64_t a0, uint64_t count, const Alphas& al,
+                       double* partial, double* chi, cudaStream_t st) {
+  switch (T) {
+    case 11: return launch_mid_t<11, A2, DBG>(psi, N, B, gx, a0, count, al, partial, chi, st);
+    case 12: return launch_mid_t<12, A2, DBG>(psi, N, B, gx, a0, count, al, partial, chi, st);
+    case 13: return launch_mid_t<13, A2, DBG>(psi, N, B, gx, a0, count, al, partial, chi, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <int L>
+cudaError_t launch_passA_t(const double2* psi, int N, uint64_t a0, int kcount, double* ws, int units, cudaStream_t st) {
+  static bool init = false;
+  if (!init) {
+    cudaError_t e = set_smem(k_passA<L>, SMEM_128K);
+    if (e != cudaSuccess) return e;
+    init = true;
+  }
+  const uint64_t items = (uint64_t)kcount << (N - 1 - L);
+  const unsigned grid = (unsigned)((items + units - 1) / units);
+  return launch_counted(LK_PASSA, st, [&] {
+    k_passA<L><<<grid, 256, SMEM_128K, st>>>(psi, N, a0, kcount, ws);
+    return cudaGetLastError();
+  });
+}
+
+cudaError_t launch_passA(const Plan& p, const double2* psi, uint64_t a0, int kcount, double* ws, cudaStream_t st) {
+  switch (p.L) {
+    case 10: return launch_passA_t<10>(psi, p.N, a0, kcount, ws, p.unitsA, st);
+    case 11: return launch_passA_t<11>(psi, p.N, a0, kcount, ws, p.unitsA, st);
+    case 12: return launch_passA_t<12>(psi, p.N, a0, kcount, ws, p.unitsA, st);
+    case 13: return launch_passA_t<13>(psi, p.N, a0, kcount, ws, p.unitsA, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <int TP, int CB, bool A2, bool DBG>
+cudaError_t launch_passB_t(const Plan& p, uint64_t a0, int kcount, const double* ws, const Alphas& al, double* partial,
+                           double* chi, cudaStream_t st) {
+  constexpr int BLK = TP >= 14 ? 512 : 256;
+  constexpr int SM = BLK * 32 * 8;
+  static bool init = false;
+  if (!init) {
+    cudaError_t e = set_smem(k_passB<TP, CB, A2, DBG>, SM);
+    if (e != cudaSuccess) return e;
+    init = true;
+  }
+  const uint64_t items = (uint64_t)kcount * 2 * (1ull << (p.L - CB));
+  const unsigned grid = (unsigned)((items + p.unitsB - 1) / p.unitsB);
+  return launch_counted(LK_PASSB, st, [&] {
+    k_passB<TP, CB, A2, DBG><<<grid, BLK, SM, st>>>(p.N, p.L, a0, kcount, ws, al, partial, chi);
+    return cudaGetLastError();
+  });
+}
+
+template <bool A2, bool DBG>
+cudaError_t launch_passB(const Plan& p, uint64_t a0, int kcount, const double* ws, const Alphas& al, double* partial,
+                         double* chi, cudaStream_t st) {
+  const int key = p.TP * 16 + p.CB;
+  switch (key) {
+#define C_(tp, cb) case tp * 16 + cb: return launch_passB_t<tp, cb, A2, DBG>(p, a0, kcount, ws, al, partial, chi, st);
+    C_(10, 6) C_(11, 6) C_(12, 6) C_(13, 6) C_(13, 5) C_(13, 4) C_(13, 3) C_(13, 2) C_(14, 2)
+#undef C_
+  }
+  return cudaErrorInvalidValue;
+}
+
+int occupancy_small(int T, const Dev& d) {
+  (void)T;
+  return 4 * d.sms;  // 256-thread CTAs, modest registers
+}
+
+// ------------------------------------------------------------------------------------------
+// the range driver: sums_dev[B][n_alpha+2] for a in [a_begin, a_end)
+// ------------------------------------------------------------------------------------------
+int run_range(const double2* psi, int N, int B, uint64_t a_begin, uint64_t a_end, const double* alpha, int n_alpha,
+              char* ws, size_t ws_bytes, double* sums_dev, cudaStream_t st) {
+  Dev d;
+  int rc = get_dev(d);
+  if (rc) return rc;
+  Plan p;
+  make_plan(N, d, p);
+  if (ws_bytes < ws_bytes_for(p, B)) return fail(SRE_EWORKSPACE, "workspace %zu < required %zu", ws_bytes, ws_bytes_for(p, B));
+  double* partial = reinterpret_cast<double*>(ws);
+  const size_t partial_doubles = p.slots * NACC * (p.kind == TWOPASS ? 1 : (size_t)B);
+  double* slab = partial + partial_doubles;
+  const uint64_t count = a_end - a_begin;
+  CK(cudaMemsetAsync(sums_dev, 0, sizeof(double) * (size_t)B * (n_alpha + 2), st));
+  if (count == 0) return SRE_OK;
+  const std::vector<Sweep> sweeps = make_sweeps(alpha, n_alpha);
+  for (const Sweep& sw : sweeps) {
+    ReduceArgs ra;
+    memset(&ra, 0, sizeof(ra));
+    ra.n_alpha = n_alpha;
+    ra.first = sw.first;
+    ra.n_this = sw.al.n;
+    ra.write_common = sw.first == 0;
+    for (int i = 0; i < MAXA; ++i) ra.scale4[i] = sw.scale4[i];
+    if (p.kind == SMALL || p.kind == MID) {
+      int gx;
+      if (p.kind == SMALL) {
+        const int G = p.T >= 5 ? 32 : (1 << p.T);
+        gx = pick_gx(count, 256 / G, B, occupancy_small(p.T, d));
+      } else {
+        gx = pick_gx(count, 256 >> (p.T - 5), B, d.sms);
+      }
+      if ((size_t)gx > p.slots) gx = (int)p.slots;
+      CK(cudaMemsetAsync(partial, 0, sizeof(double) * (size_t)gx * B * NACC, st));
+      cudaError_t e;
+      if (p.kind == SMALL)
+        e = sw.a2 ? launch_small<true, false>(p.T, psi, N, B, gx, a_begin, count, sw.al, partial, nullptr, st)
+                  : launch_small<false, false>(p.T, psi, N, B, gx, a_begin, count, sw.al, partial, nullptr, st);
+      else
+        e = sw.a2 ? launch_mid<true, false>(p.T, psi, N, B, gx, a_begin, count, sw.al, partial, nullptr, st)
+                  : launch_mid<false, false>(p.T, psi, N, B, gx, a_begin, count, sw.al, partial, nullptr, st);
+      if (e != cudaSuccess) return fail(SRE_ECUDA, "launch: %s", cudaGetErrorString(e));
+      ra.nslots = gx;
+      CK(launch_counted(LK_AUX, st, [&] { k_reduce<<<B, 32, 0, st>>>(partial, ra, sums_dev); return cudaGetLastError(); }));
+    } else {
+      for (int s = 0; s < B; ++s) {
+        const double2* ps = psi + ((size_t)s << N);
+        CK(cudaMemsetAsync(partial, 0, sizeof(double) * p.slots * NACC, st));
+        for (uint64_t a = a_begin; a < a_end; a += (uint64_t)p.K) {
+          const int kc = (int)((a_end - a) < (uint64_t)p.K ? (a_end - a) : (uint64_t)p.K);
+          cudaError_t e = launch_passA(p, ps, a, kc, slab, st);
+          if (e != cudaSuccess) return fail(SRE_ECUDA, "passA: %s", cudaGetErrorString(e));
+          e = sw.a2 ? launch_passB<true, false>(p, a, kc, slab, sw.al, partial, nullptr, st)
+                    : launch_passB<false, false>(p, a, kc, slab, sw.al, partial, nullptr, st);
+          if (e != cudaSuccess) return fail(SRE_ECUDA, "passB: %s", cudaGetErrorString(e));
+        }
+        ra.nslots = (int)p.slots;
+        CK(launch_counted(LK_AUX, st, [&] {
+          k_reduce<<<1, 32, 0, st>>>(partial, ra, sums_dev + (size_t)s * (n_alpha + 2));
+          return cudaGetLastError();
+        }));
+      }
+    }
+  }
+  return SRE_OK;
+}
+
+int validate_common(const void* psi, int N, int B, const double* alpha, int n_alpha) {
+  if (!psi) return fail(SRE_EINVAL, "psi is NULL");
+  if (N < 1 || N > SRE_MAX_N) return fail(SRE_ERANGE, "N=%d outside [1, %d]", N, SRE_MAX_N);
+  if (B < 1) return fail(SRE_ERANGE, "B=%d < 1", B);
+  if (!alpha) return fail(SRE_EINVAL, "alpha is NULL");
+  if (n_alpha < 1 || n_alpha > SRE_MAX_ALPHA) return fail(SRE_EINVAL, "n_alpha=%d outside [1, %d]", n_alpha, SRE_MAX_ALPHA);
+  for (int i = 0; i < n_alpha; ++i)
+    if (!(alpha[i] > 0.0) || !std::isfinite(alpha[i])) return fail(SRE_EINVAL, "alpha[%d]=%g must be finite and > 0", i, alpha[i]);
+  if (reinterpret_cast<uintptr_t>(psi) % 16) return fail(SRE_EINVAL, "psi not 16-byte aligned");
+  return SRE_OK;
+}
+
+int is_device_ptr(const void* ptr, bool& dev) {
+  cudaPointerAttributes at;
+  cudaError_t e = cudaPointerGetAttributes(&at, ptr);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    dev = false;
+    return SRE_OK;
+  }
+  dev = (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged);
+  return SRE_OK;
+}
+
+// internal cached device buffers for the synchronous calls
+struct Cache {
+  std::mutex mu;
+  char* ws = nullptr;
+  size_t ws_bytes = 0;
+  char* in = nullptr;
+  size_t in_bytes = 0;
+  int dev = -1;
+};
+Cache g_cache;
+
+int cache_get(char** buf, size_t* have, size_t need) {
+  if (*have >= need) return SRE_OK;
+  if (*buf) cudaFree(*buf);
+  *buf = nullptr;
+  *have = 0;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(buf), need);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(SRE_ENOMEM, "cudaMalloc(%zu): %s", need, cudaGetErrorString(e));
+  }
+  *have = need;
+  return SRE_OK;
+}
+
+int exact_impl(const void* psi, int N, int B, const double* alpha, int n_alpha, double* out_M, double* out_ln) {
+  int rc = validate_common(psi, N, B, alpha, n_alpha);
+  if (rc) return rc;
+  if (!out_M) return fail(SRE_EINVAL, "out_M is NULL");
+  Dev d;
+  rc = get_dev(d);
+  if (rc) return rc;
+  bool dev_ptr = false;
+  is_device_ptr(psi, dev_ptr);
+  std::lock_guard<std::mutex> lk(g_cache.mu);
+  if (g_cache.dev != d.id) {  // device switched: drop cached buffers of the old device
+    g_cache.ws = nullptr; g_cache.ws_bytes = 0; g_cache.in = nullptr; g_cache.in_bytes = 0; g_cache.dev = d.id;
+  }
+  Plan p;
+  make_plan(N, d, p);
+  const size_t need = ws_bytes_for(p, B) + sizeof(double) * ((size_t)B * (n_alpha + 2) + (size_t)B);
+  rc = cache_get(&g_cache.ws, &g_cache.ws_bytes, need);
+  if (rc) return rc;
+  cudaStream_t st = 0;
+  const double2* dpsi = reinterpret_cast<const double2*>(psi);
+  const size_t psi_bytes = ((size_t)B << N) * sizeof(double2);
+  if (!dev_ptr) {
+    rc = cache_get(&g_cache.in, &g_cache.in_bytes, psi_bytes);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(g_cache.in, psi, psi_bytes, cudaMemcpyHostToDevice, st));
+    dpsi = reinterpret_cast<const double2*>(g_cache.in);
+  }
+  double* sums = reinterpret_cast<double*>(g_cache.ws + ws_bytes_for(p, B));
+  double* norms = sums + (size_t)B * (n_alpha + 2);
+  // norm check (reading C6)
+  {
+    double* part = reinterpret_cast<double*>(g_cache.ws) + p.slots * NACC * (p.kind == TWOPASS ? 1 : (size_t)B) +
+                   p.slab_doubles;  // the norm area of ws_bytes_for
+    const int nb = 64;
+    dim3 g(nb, B);
+    CK(launch_counted(LK_AUX, st, [&] { k_norm2_partial<<<g, 256, 0, st>>>(dpsi, N, part); return cudaGetLastError(); }));
+    CK(launch_counted(LK_AUX, st, [&] { k_norm2_final<<<B, 32, 0, st>>>(part, nb, norms); return cudaGetLastError(); }));
+    std::vector<double> hn(B);
+    CK(cudaMemcpyAsync(hn.data(), norms, sizeof(double) * B, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int s = 0; s < B; ++s)
+      if (!(std::fabs(hn[s] - 1.0) <= 1e-8)) return fail(SRE_ENOTNORM, "state %d: ||psi||^2 = %.17g", s, hn[s]);
+  }
+  rc = run_range(dpsi, N, B, 0, 1ull << N, alpha, n_alpha, g_cache.ws, ws_bytes_for(p, B), sums, st);
+  if (rc) return rc;
+  std::vector<double> hs((size_t)B * (n_alpha + 2));
+  CK(cudaMemcpyAsync(hs.data(), sums, sizeof(double) * hs.size(), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return sre_finalize(hs.data(), N, B, alpha, n_alpha, out_M, out_ln);
+}
+
+}  // namespace
+
+// ==========================================================================================
+// exported C ABI
+// ==========================================================================================
+extern "C" {
+
+const char* sre_status_string(int code) {
+  switch (code) {
+    case SRE_OK: return "ok";
+    case SRE_EINVAL: return "invalid argument";
+    case SRE_ERANGE: return "size out of range";
+    case SRE_ENOTNORM: return "state not normalised";
+    case SRE_EWORKSPACE: return "workspace too small";
+    case SRE_ENOMEM: return "device allocation failed";
+    case SRE_ECUDA: return "CUDA error";
+    case SRE_EINTERNAL: return "internal error";
+    case SRE_ENODEV: return "no sm_100 device";
+  }
+  return "unknown status";
+}
+
+const char* sre_last_error(void) { return g_err; }
+
+int sre_version(void) { return 100; }
+
+size_t sre_workspace_size(int N, int B, int n_alpha) {
+  if (N < 1 || N > SRE_MAX_N || B < 1 || n_alpha < 1 || n_alpha > SRE_MAX_ALPHA) return 0;
+  Dev d;  // plan does not depend on the device
+  Plan p;
+  make_plan(N, d, p);
+  return ws_bytes_for(p, B);
+}
+
+int sre_exact(const void* psi, int N, const double* alpha, int n_alpha, double* out_M, double* out_lost_norm) {
+  g_err[0] = 0;
+  return exact_impl(psi, N, 1, alpha, n_alpha, out_M, out_lost_norm);
+}
+
+int sre_exact_batched(const void* psi, int N, int B, const double* alpha, int n_alpha, double* out_M,
+                      double* out_lost_norm) {
+  g_err[0] = 0;
+  return exact_impl(psi, N, B, alpha, n_alpha, out_M, out_lost_norm);
+}
+
+int sre_partial_sums(const void* psi, int N, int B, uint64_t a_begin, uint64_t a_end, const double* alpha, int n_alpha,
+                     void* workspace, size_t ws_bytes, double* sums_dev, void* stream) {
+  g_err[0] = 0;
+  int rc = validate_common(psi, N, B, alpha, n_alpha);
+  if (rc) return rc;
+  if (!workspace) return fail(SRE_EINVAL, "workspace is NULL");
+  if (!sums_dev) return fail(SRE_EINVAL, "sums_dev is NULL");
+  if (a_begin > a_end || a_end > (1ull << N)) return fail(SRE_ERANGE, "range [%llu, %llu) outside [0, 2^%d]",
+                                                          (unsigned long long)a_begin, (unsigned long long)a_end, N);
+  bool dv = false;
+  is_device_ptr(psi, dv);
+  if (!dv) return fail(SRE_EINVAL, "psi must be a device pointer");
+  is_device_ptr(sums_dev, dv);
+  if (!dv) return fail(SRE_EINVAL, "sums_dev must be a device pointer");
+  return run_range(reinterpret_cast<const double2*>(psi), N, B, a_begin, a_end, alpha, n_alpha,
+                   reinterpret_cast<char*>(workspace), ws_bytes, sums_dev, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int sre_finalize(const double* sums, int N, int B, const double* alpha, int n_alpha, double* out_M,
+                 double* out_lost_norm) {
+  if (!sums || !alpha || !out_M) return fail(SRE_EINVAL, "NULL argument");
+  if (N < 1 || N > SRE_MAX_N || B < 1) return fail(SRE_ERANGE, "N=%d B=%d", N, B);
+  if (n_alpha < 1 || n_alpha > SRE_MAX_ALPHA) return fail(SRE_EINVAL, "n_alpha=%d", n_alpha);
+  const double D = std::ldexp(1.0, N);
+  for (int s = 0; s < B; ++s) {
+    const double* r = sums + (size_t)s * (n_alpha + 2);
+    for (int i = 0; i < n_alpha; ++i) {
+      if (alpha[i] == 1.0)
+        out_M[(size_t)s * n_alpha + i] = -(r[n_alpha + 1] / std::log(2.0)) / D;  // reading C4
+      else
+        out_M[(size_t)s * n_alpha + i] = std::log2(r[i] / D) / (1.0 - alpha[i]);  // Eq. (2)
+    }
+    if (out_lost_norm) out_lost_norm[s] = 1.0 - r[n_alpha] / D;
+  }
+  return SRE_OK;
+}
+
+int sre_norm2(const void* psi, int N, int B, double* out_dev, void* stream) {
+  if (!psi || !out_dev) return fail(SRE_EINVAL, "NULL argument");
+  if (N < 1 || N > SRE_MAX_N || B < 1) return fail(SRE_ERANGE, "N=%d B=%d", N, B);
+  // single-block-per-state reduction straight into out_dev (no workspace needed)
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  dim3 g(1, B);
+  CK(launch_counted(LK_AUX, st, [&] {
+    k_norm2_partial<<<g, 1024, 0, st>>>(reinterpret_cast<const double2*>(psi), N, out_dev);
+    return cudaGetLastError();
+  }));
+  return SRE_OK;
+}
+
+int sre_chi(const void* psi, int N, uint64_t a, double* chi_dev, void* stream) {
+  g_err[0] = 0;
+  double one = 2.0;
+  int rc = validate_common(psi, N, 1, &one, 1);
+  if (rc) return rc;
+  if (!chi_dev) return fail(SRE_EINVAL, "chi_dev is NULL");
+  if (a >= (1ull << N)) return fail(SRE_ERANGE, "a out of range");
+  Dev d;
+  rc = get_dev(d);
+  if (rc) return rc;
+  Plan p;
+  make_plan(N, d, p);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const double2* dpsi = reinterpret_cast<const double2*>(psi);
+  Alphas al;
+  memset(&al, 0, sizeof(al));
+  al.n = 1;
+  cudaError_t e = cudaSuccess;
+  if (p.kind == SMALL) {
+    e = launch_small<false, true>(p.T, dpsi, N, 1, 1, a, 1, al, nullptr, chi_dev, st);
+  } else if (p.kind == MID) {
+    e = launch_mid<false, true>(p.T, dpsi, N, 1, 1, a, 1, al, nullptr, chi_dev, st);
+  } else {
+    std::lock_guard<std::mutex> lk(g_cache.mu);
+    if (g_cache.dev != d.id) { g_cache.ws = nullptr; g_cache.ws_bytes = 0; g_cache.in = nullptr; g_cache.in_bytes = 0; g_cache.dev = d.id; }
+    rc = cache_get(&g_cache.ws, &g_cache.ws_bytes, ws_bytes_for(p, 1));
+    if (rc) return rc;
+    double* slab = reinterpret_cast<double*>(g_cache.ws) + p.slots * NACC;
+    e = launch_passA(p, dpsi, a, 1, slab, st);
+    if (e == cudaSuccess) e = launch_passB<false, true>(p, a, 1, slab, al, nullptr, chi_dev, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  }
+  if (e != cudaSuccess) return fail(SRE_ECUDA, "sre_chi: %s", cudaGetErrorString(e));
+  return SRE_OK;
+}
+
+uint64_t sre_launch_count(void) { return g_launches.load(); }
+
+int sre_profile_begin(int stride) {
+  std::lock_guard<std::mutex> lk(g_prof.mu);
+  if (stride < 1) return fail(SRE_EINVAL, "stride %d < 1", stride);
+  for (int k = 0; k < LK_N; ++k) {
+    for (auto& pr : g_prof.timed[k]) { g_prof.pool.push_back(pr.first); g_prof.pool.push_back(pr.second); }
+    g_prof.timed[k].clear();
+    g_prof.launched[k] = 0;
+  }
+  g_prof.stride = stride;
+  g_prof.on = true;
+  return SRE_OK;
+}
+
+int sre_profile_end(double* ms_sum, uint64_t* n_timed, uint64_t* n_launched) {
+  std::lock_guard<std::mutex> lk(g_prof.mu);
+  g_prof.on = false;
+  for (int k = 0; k < LK_N; ++k) {
+    double acc = 0.0;
+    for (auto& pr : g_prof.timed[k]) {
+      float ms = 0.f;
+      CK(cudaEventSynchronize(pr.second));
+      CK(cudaEventElapsedTime(&ms, pr.first, pr.second));
+      acc += ms;
+    }
+    if (ms_sum) ms_sum[k] = acc;
+    if (n_timed) n_timed[k] = g_prof.timed[k].size();
+    if (n_launched) n_launched[k] = g_prof.launched[k];
+  }
+  return SRE_OK;
+}
+
+}  // extern "C"

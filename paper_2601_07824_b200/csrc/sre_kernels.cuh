@@ -1,0 +1,476 @@
+// sre_kernels.cuh -- sm_100a kernels for the exact stabilizer Renyi entropy (Alg. 2 of
+// arXiv:2601.07824).
+//
+// Half-length reformulation (reading C3):
+//   For an X-string a != 0 with pivot p = highest set bit of a, pair x with x^a (x_p = 0).
+//   v_x = conj(psi_{x^a}) psi_x satisfies v_{x^a} = conj(v_x), hence
+//     chi_b(a) = 2 Re-hat(b')      if a.b even,   chi_b(a) = 2i Im-hat(b')   if a.b odd,
+//   where b' is b with bit p removed and Re-hat / Im-hat are the unnormalised Walsh-Hadamard
+//   transforms over the N-1 remaining bits of A_y = Re v_{x(y)}, B_y = Im v_{x(y)},
+//   x(y) = y with a 0 inserted at bit p.  Every |chi_b| is 2|y| for exactly one output y of the
+//   two real (N-1)-bit transforms.  For a = 0 (v real), the pivot butterfly is applied at
+//   generation: A_y = (|psi_x0|^2 + |psi_x1|^2)/2, B_y = (|psi_x0|^2 - |psi_x1|^2)/2, x1 = x0 + 2^{N-1},
+//   so again |chi| = 2|y|.  Kernels accumulate t' = y^2; the reduce kernel rescales t = 4 t'.
+//
+// Transform engine: a "unit" of NT = 2^(T-5) threads holds a 2^T-point real vector, 32 values
+// per thread.  Round k puts 5 index bits [s_k, s_k+5) in the register index j (radix-32
+// butterflies in registers); between rounds the unit transposes through shared memory with
+// the XOR swizzle swz(e) = e ^ ((e >> 5) & 15) (conflict-free for every round layout).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <type_traits>
+
+namespace sre {
+
+constexpr int MAXA = 4;          // Renyi indices per sweep (more are done in extra sweeps)
+constexpr int NACC = MAXA + 2;   // [0,MAXA) alpha sums, [MAXA] purity, [MAXA+1] t ln t
+
+struct Alphas {
+  int n;                // alphas in this sweep
+  int need_log;         // any alpha == 1
+  int kind[MAXA];       // 0: integer exponent iexp[i] >= 1, 2: general real power
+  int iexp[MAXA];
+  double alpha[MAXA];
+};
+
+// ------------------------------------------------------------------------------------------
+// small helpers
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t ins0(uint64_t y, int p) {  // insert a 0 bit at position p
+  const uint64_t lo = y & ((1ull << p) - 1ull);
+  return lo | ((y >> p) << (p + 1));
+}
+__device__ __forceinline__ uint32_t lay(uint32_t t, uint32_t j, int s) {
+  return (t & ((1u << s) - 1u)) | (j << s) | ((t >> s) << (s + 5));
+}
+__device__ __forceinline__ uint32_t swz(uint32_t e) { return e ^ ((e >> 5) & 15u); }
+
+struct Round { int s, rlo, rhi; };
+__host__ __device__ constexpr int nrounds(int T, int LO) {
+  int hi = T, n = 0;
+  while (hi > LO) { hi = (hi - LO >= 5) ? hi - 5 : LO; ++n; }
+  return n;
+}
+__host__ __device__ constexpr Round round_k(int T, int LO, int k) {
+  int hi = T;
+  for (int i = 0;; ++i) {
+    Round r{0, 0, 0};
+    if (hi - LO >= 5) { r.s = hi - 5; r.rlo = 0; r.rhi = 5; }
+    else { r.s = hi - 5 > 0 ? hi - 5 : 0; r.rlo = LO - r.s; r.rhi = hi - r.s; }
+    if (i == k) return r;
+    hi = (hi - LO >= 5) ? hi - 5 : LO;
+  }
+}
+
+template <int RLO, int RHI>
+__device__ __forceinline__ void bfly32(double (&v)[32]) {
+#pragma unroll
+  for (int b = RLO; b < RHI; ++b) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      if ((i >> b) & 1) continue;
+      const int k = i | (1 << b);
+      const double u = v[i], w = v[k];
+      v[i] = u + w;
+      v[k] = u - w;
+    }
+  }
+}
+
+struct BarWarp { __device__ __forceinline__ void sync() const { __syncwarp(); } };
+struct BarNamed {
+  int id, n;
+  __device__ __forceinline__ void sync() const {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+  }
+};
+struct BarCta { __device__ __forceinline__ void sync() const { __syncthreads(); } };
+
+// Rounds K..end of the transform of NP planes (each a 2^T vector in its own 2^T smem slice).
+// On entry the registers hold round K-1's layout (or round 0's with butterflies pending if
+// K == 0); on exit the final round's layout with all butterflies done.
+template <int T, int LO, int K, int NP, class Bar>
+struct Rounds {
+  __device__ __forceinline__ static void run(double (&v)[NP][32], double* sm, uint32_t t, const Bar& bar) {
+    constexpr int NR = nrounds(T, LO);
+    if constexpr (K < NR) {
+      constexpr Round r = round_k(T, LO, K);
+      if constexpr (K > 0) {
+        constexpr Round q = round_k(T, LO, K - 1);
+        bar.sync();
+#pragma unroll
+        for (int pl = 0; pl < NP; ++pl)
+#pragma unroll
+          for (int j = 0; j < 32; ++j) sm[pl * (1 << T) + swz(lay(t, j, q.s))] = v[pl][j];
+        bar.sync();
+#pragma unroll
+        for (int pl = 0; pl < NP; ++pl)
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[pl][j] = sm[pl * (1 << T) + swz(lay(t, j, r.s))];
+      }
+#pragma unroll
+      for (int pl = 0; pl < NP; ++pl) bfly32<r.rlo, r.rhi>(v[pl]);
+      Rounds<T, LO, K + 1, NP, Bar>::run(v, sm, t, bar);
+    }
+  }
+};
+template <int T, int LO>
+__host__ __device__ constexpr int final_s() { return round_k(T, LO, nrounds(T, LO) - 1).s; }
+
+// ------------------------------------------------------------------------------------------
+// epilogue: power sums of t' = y^2 (DESIGN "Epilogue"); A2 = compile-time single alpha == 2
+// ------------------------------------------------------------------------------------------
+template <bool A2>
+struct Epi {
+  __device__ __forceinline__ static void add(double (&acc)[NACC], double y, const Alphas& al) {
+    const double t = y * y;
+    acc[MAXA] += t;
+    if constexpr (A2) {
+      acc[0] = fma(t, t, acc[0]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < MAXA; ++i) {
+        if (i < al.n) {
+          if (al.kind[i] == 0) {
+            double pw = t;
+            for (int k = 1; k < al.iexp[i]; ++k) pw *= t;
+            acc[i] += pw;
+          } else {
+            acc[i] += (t > 0.0) ? exp(al.alpha[i] * log(t)) : 0.0;
+          }
+        }
+      }
+      if (al.need_log) acc[MAXA + 1] += (t > 0.0) ? t * log(t) : 0.0;
+    }
+  }
+};
+
+// Block reduction of the NACC accumulators; thread 0 adds them to partial[slot].
+__device__ __forceinline__ void block_flush(double (&acc)[NACC], double* partial, int slot) {
+  __shared__ double red[32][NACC];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int i = 0; i < NACC; ++i) {
+    double x = acc[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    acc[i] = x;
+  }
+  __syncthreads();
+  if (lane == 0)
+#pragma unroll
+    for (int i = 0; i < NACC; ++i) red[w][i] = acc[i];
+  __syncthreads();
+  if (threadIdx.x < NACC) {
+    double s = 0.0;
+    for (int k = 0; k < nw; ++k) s += red[k][threadIdx.x];
+    partial[(size_t)slot * NACC + threadIdx.x] += s;
+  }
+}
+
+// Generation of (A_y, B_y) for the half-index y of X-string a (pivot p; a == 0 special).
+__device__ __forceinline__ void gen_pair(const double2* __restrict__ psi, uint64_t y, uint64_t a, int p,
+                                         int N, double& A, double& B) {
+  if (a != 0) {
+    const uint64_t x = ins0(y, p);
+    const double2 q = __ldg(psi + x);        // alpha_x = psi_x
+    const double2 r = __ldg(psi + (x ^ a));  // beta_x = psi_{x^a}
+    A = fma(r.x, q.x, r.y * q.y);            // Re conj(beta) alpha
+    B = fma(r.x, q.y, -(r.y * q.x));         // Im conj(beta) alpha
+  } else {
+    const uint64_t x0 = y, x1 = y | (1ull << (N - 1));
+    const double2 q0 = __ldg(psi + x0), q1 = __ldg(psi + x1);
+    const double n0 = fma(q0.x, q0.x, q0.y * q0.y), n1 = fma(q1.x, q1.x, q1.y * q1.y);
+    A = (n0 + n1) * 0.5;
+    B = (n0 - n1) * 0.5;
+  }
+}
+__device__ __forceinline__ int pivot_of(uint64_t a, int N) { return a ? 63 - __clzll((long long)a) : N - 1; }
+
+// chi_b from an output y of plane pl at half-index bq (debug path, natural b order).
+__device__ __forceinline__ void chi_store(double* chi, uint64_t a, int p, int pl, uint64_t bq, double y) {
+  uint64_t b0 = ins0(bq, p), b;
+  double re = 2.0 * y, im = 0.0;
+  if (a == 0) {
+    b = b0 | ((uint64_t)pl << p);
+  } else {
+    const uint64_t arest = a & ~(1ull << p);
+    const int par = __popcll(arest & b0) & 1;  // parity of a.b with b_p = 0
+    const int bp = pl == 0 ? par : (par ^ 1);  // plane A <-> a.b even, plane B <-> odd
+    b = b0 | ((uint64_t)bp << p);
+    if (pl == 1) { im = re; re = 0.0; }
+  }
+  chi[2 * b] = re;
+  chi[2 * b + 1] = im;
+}
+
+// ------------------------------------------------------------------------------------------
+// k_small: T = N-1 <= 10.  Group of G = min(32, 2^T) lanes per X-string, R = 2^T/G values
+// per plane per lane; register bits then shuffle bits.  One pass, no workspace.
+// ------------------------------------------------------------------------------------------
+template <int T, bool A2, bool DEBUG>
+__global__ void __launch_bounds__(256) k_small(const double2* __restrict__ psi_all, int N, uint64_t a0,
+                                               uint64_t count, Alphas al, double* partial, double* chi) {
+  constexpr int G = T >= 5 ? 32 : (1 << T);
+  constexpr int LG = T >= 5 ? 5 : T;
+  constexpr int R = (1 << T) / G;
+  constexpr int PER_CTA = 256 / G;
+  const double2* psi = psi_all + ((size_t)blockIdx.y << N);
+  const int g = threadIdx.x & (G - 1);
+  double acc[NACC];
+#pragma unroll
+  for (int i = 0; i < NACC; ++i) acc[i] = 0.0;
+  const uint64_t stride = (uint64_t)gridDim.x * PER_CTA;
+  const uint64_t warp_first = (uint64_t)blockIdx.x * PER_CTA + (threadIdx.x >> 5) * (32 / G);
+  for (uint64_t base = warp_first; base < count; base += stride) {
+    const uint64_t item = base + ((threadIdx.x & 31) >> LG);
+    const bool valid = item < count;
+    const uint64_t a = a0 + item;
+    const int p = pivot_of(a, N);
+    double A[R], B[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      A[j] = 0.0; B[j] = 0.0;
+      if (valid) gen_pair(psi, (uint64_t)g + (uint64_t)G * j, a, p, N, A[j], B[j]);
+    }
+#pragma unroll
+    for (int h = 1; h < R; h <<= 1)
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        if (i & h) continue;
+        double u = A[i], w = A[i + h]; A[i] = u + w; A[i + h] = u - w;
+        u = B[i]; w = B[i + h]; B[i] = u + w; B[i + h] = u - w;
+      }
+#pragma unroll
+    for (int m = 1; m < G; m <<= 1) {
+      const bool up = (g & m) != 0;
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const double pa = __shfl_xor_sync(0xffffffffu, A[i], m, G);
+        const double pb = __shfl_xor_sync(0xffffffffu, B[i], m, G);
+        A[i] = up ? pa - A[i] : A[i] + pa;
+        B[i] = up ? pb - B[i] : B[i] + pb;
+      }
+    }
+    if (valid) {
+      if constexpr (DEBUG) {
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          chi_store(chi, a, p, 0, (uint64_t)g + (uint64_t)G * j, A[j]);
+          chi_store(chi, a, p, 1, (uint64_t)g + (uint64_t)G * j, B[j]);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < R; ++j) { Epi<A2>::add(acc, A[j], al); Epi<A2>::add(acc, B[j], al); }
+      }
+    }
+  }
+  if constexpr (!DEBUG) block_flush(acc, partial, blockIdx.y * gridDim.x + blockIdx.x);
+}
+
+// ------------------------------------------------------------------------------------------
+// k_mid: 11 <= T = N-1 <= 13.  A unit of NT = 2^(T-5) threads owns one X-string: 32 values of
+// each plane per thread, smem 2 * 2^T doubles per unit.  CTA = 256 threads.
+// ------------------------------------------------------------------------------------------
+template <int T>
+__device__ __forceinline__ void unit_gen(const double2* __restrict__ psi, uint64_t ybase, uint64_t a, int p, int N,
+                                         uint32_t t, double (&v)[2][32]) {
+  constexpr int NT = 1 << (T - 5);
+#pragma unroll
+  for (int j = 0; j < 32; ++j) gen_pair(psi, ybase + t + (uint64_t)NT * j, a, p, N, v[0][j], v[1][j]);
+}
+
+template <int T, class F>
+__device__ __forceinline__ void with_unit_bar(F&& f) {
+  constexpr int NT = 1 << (T - 5);
+  if constexpr (NT == 32) f(BarWarp{});
+  else f(BarNamed{1 + (int)(threadIdx.x / NT), NT});
+}
+
+template <int T, bool A2, bool DEBUG>
+__global__ void __launch_bounds__(256, 1) k_mid(const double2* __restrict__ psi_all, int N, uint64_t a0,
+                                                uint64_t count, Alphas al, double* partial, double* chi) {
+  constexpr int NT = 1 << (T - 5);
+  constexpr int UPC = 256 / NT;
+  extern __shared__ double smem[];
+  const double2* psi = psi_all + ((size_t)blockIdx.y << N);
+  const uint32_t t = threadIdx.x & (NT - 1);
+  const int unit = threadIdx.x / NT;
+  double* sm = smem + (size_t)unit * 2 * (1 << T);
+  double acc[NACC];
+#pragma unroll
+  for (int i = 0; i < NACC; ++i) acc[i] = 0.0;
+  for (uint64_t item = (uint64_t)blockIdx.x * UPC + unit; item < count; item += (uint64_t)gridDim.x * UPC) {
+    const uint64_t a = a0 + item;
+    const int p = pivot_of(a, N);
+    double v[2][32];
+    unit_gen<T>(psi, 0, a, p, N, t, v);
+    with_unit_bar<T>([&](const auto& bar) { Rounds<T, 0, 0, 2, std::decay_t<decltype(bar)>>::run(v, sm, t, bar); });
+    if constexpr (DEBUG) {
+      constexpr int sf = final_s<T, 0>();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        chi_store(chi, a, p, 0, lay(t, j, sf), v[0][j]);
+        chi_store(chi, a, p, 1, lay(t, j, sf), v[1][j]);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) { Epi<A2>::add(acc, v[0][j], al); Epi<A2>::add(acc, v[1][j], al); }
+    }
+  }
+  if constexpr (!DEBUG) block_flush(acc, partial, blockIdx.y * gridDim.x + blockIdx.x);
+}
+
+// ------------------------------------------------------------------------------------------
+// Two-pass path, T = N-1 >= 14 = L + H.  Workspace per X-string: planes [2][2^H][2^L] doubles.
+// Pass A: a unit (NT = 2^(L-5) threads) generates one row y_h of both planes and transforms
+// the L low bits; writes row positions pos = t + NT*j (position pos holds b_l = lay(t,j,sL)).
+// ------------------------------------------------------------------------------------------
+template <int L>
+__global__ void __launch_bounds__(256, 1) k_passA(const double2* __restrict__ psi, int N, uint64_t a0,
+                                                  int kcount, double* __restrict__ ws) {
+  constexpr int NT = 1 << (L - 5);
+  constexpr int UPC = 256 / NT;
+  extern __shared__ double smem[];
+  const int H = N - 1 - L;
+  const uint32_t t = threadIdx.x & (NT - 1);
+  const int unit = threadIdx.x / NT;
+  double* sm = smem + (size_t)unit * 2 * (1 << L);
+  const uint64_t item = (uint64_t)blockIdx.x * UPC + unit;  // item = k * 2^H + y_h
+  const uint64_t rows = 1ull << H;
+  if (item >= (uint64_t)kcount * rows) return;  // whole units only; bars are per unit
+  const int k = (int)(item >> H);
+  const uint64_t yh = item & (rows - 1);
+  const uint64_t a = a0 + (uint64_t)k;
+  const int p = pivot_of(a, N);
+  double v[2][32];
+  unit_gen<L>(psi, yh << L, a, p, N, t, v);
+  with_unit_bar<L>([&](const auto& bar) { Rounds<L, 0, 0, 2, std::decay_t<decltype(bar)>>::run(v, sm, t, bar); });
+  const size_t plane = (size_t)1 << (N - 1);
+  double* w0 = ws + (size_t)k * 2 * plane + (yh << L) + t;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    __stcg(w0 + (size_t)NT * j, v[0][j]);
+    __stcg(w0 + plane + (size_t)NT * j, v[1][j]);
+  }
+}
+
+// Pass B: a unit (NT = 2^(TP-5) threads, TP = CB + H) reads a slab of C = 2^CB columns x 2^H
+// rows of one plane, transforms the H row bits, and accumulates the epilogue.
+template <int TP, int CB, bool A2, bool DEBUG>
+__global__ void __launch_bounds__(TP >= 14 ? 512 : 256, 1) k_passB(int N, int L, uint64_t a0, int kcount,
+                                                                   const double* __restrict__ ws, Alphas al,
+                                                                   double* partial, double* chi) {
+  constexpr int NT = 1 << (TP - 5);
+  constexpr int BLK = TP >= 14 ? 512 : 256;
+  constexpr int UPC = BLK / NT;
+  constexpr int H = TP - CB;
+  extern __shared__ double smem[];
+  const uint32_t t = threadIdx.x & (NT - 1);
+  const int unit = threadIdx.x / NT;
+  double* sm = smem + (size_t)unit * (1 << TP);
+  double acc[NACC];
+#pragma unroll
+  for (int i = 0; i < NACC; ++i) acc[i] = 0.0;
+  const uint64_t slabs = 1ull << (L - CB);  // per plane
+  const uint64_t item = (uint64_t)blockIdx.x * UPC + unit;  // item = (k*2 + plane) * slabs + slab
+  if (item < (uint64_t)kcount * 2 * slabs) {
+    const uint64_t kp = item / slabs, slab = item % slabs;
+    const size_t plane_sz = (size_t)1 << (N - 1);
+    const double* src = ws + kp * plane_sz + (slab << CB);
+    double v[1][32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const uint32_t e = t + (uint32_t)NT * j;  // round-0 layout
+      v[0][j] = __ldcg(src + ((size_t)(e >> CB) << L) + (e & ((1u << CB) - 1u)));
+    }
+    with_unit_bar<TP>([&](const auto& bar) { Rounds<TP, CB, 0, 1, std::decay_t<decltype(bar)>>::run(v, sm, t, bar); });
+    if constexpr (DEBUG) {
+      const uint64_t a = a0 + kp / 2;
+      const int p = pivot_of(a, N);
+      const int pl = (int)(kp & 1);
+      constexpr int sf = final_s<TP, CB>();
+      const int ntA = 1 << (L - 5);
+      const int sA = L == 10 ? final_s<10, 0>() : L == 11 ? final_s<11, 0>() : L == 12 ? final_s<12, 0>() : final_s<13, 0>();
+      for (int j = 0; j < 32; ++j) {
+        const uint32_t e = lay(t, j, sf);
+        const uint64_t bh = e >> CB;
+        const uint32_t pos = (uint32_t)(slab << CB) + (e & ((1u << CB) - 1u));
+        const uint64_t bl = lay(pos & (ntA - 1), pos / ntA, sA);
+        chi_store(chi, a, p, pl, (bh << L) | bl, v[0][j]);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) Epi<A2>::add(acc, v[0][j], al);
+    }
+  }
+  (void)H;
+  if constexpr (!DEBUG) block_flush(acc, partial, blockIdx.x);
+}
+
+// ------------------------------------------------------------------------------------------
+// reduction of per-CTA partials (fixed order) + rescale t = 4 t' (DESIGN "Half-length").
+//   out[s*(n+2)+i] = scale_i * sum_slot partial[s][slot][i]
+// ------------------------------------------------------------------------------------------
+struct ReduceArgs {
+  int nslots;       // partial slots per state
+  int n_alpha;      // total alphas of the call (row stride n_alpha + 2)
+  int first;        // index of this sweep's first alpha
+  int n_this;       // alphas in this sweep
+  int write_common; // 1: also write purity and t ln t (sweep 0)
+  double scale4[MAXA];  // 4^alpha_i
+};
+__global__ void k_reduce(const double* __restrict__ partial, ReduceArgs r, double* out) {
+  // one block (one warp) per state; column sums over slots in fixed order
+  const int s = blockIdx.x;
+  const double* base = partial + (size_t)s * r.nslots * NACC;
+  __shared__ double col[NACC];
+  const int i = threadIdx.x;
+  if (i < NACC) {
+    double acc = 0.0;
+    for (int k = 0; k < r.nslots; ++k) acc += base[(size_t)k * NACC + i];
+    col[i] = acc;
+  }
+  __syncwarp();
+  if (i == 0) {
+    double* o = out + (size_t)s * (r.n_alpha + 2);
+    for (int k = 0; k < r.n_this; ++k) o[r.first + k] = col[k] * r.scale4[k];
+    if (r.write_common) {
+      o[r.n_alpha] = 4.0 * col[MAXA];
+      // t = 4 t':  sum t ln t = 4 sum t' ln t' + 4 ln(4) sum t'
+      o[r.n_alpha + 1] = 4.0 * col[MAXA + 1] + 4.0 * 1.3862943611198906 * col[MAXA];
+    }
+  }
+}
+
+// sum_x |psi_x|^2 per state (for the norm check), fixed-order block reduce then host/tiny sum
+__global__ void k_norm2_partial(const double2* __restrict__ psi, int N, double* part) {
+  const double2* ps = psi + ((size_t)blockIdx.y << N);
+  const uint64_t n = 1ull << N;
+  double acc = 0.0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const double2 q = __ldg(ps + i);
+    acc = fma(q.x, q.x, fma(q.y, q.y, acc));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  __shared__ double red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) s += red[k];
+    part[(size_t)blockIdx.y * gridDim.x + blockIdx.x] = s;
+  }
+}
+__global__ void k_norm2_final(const double* __restrict__ part, int nb, double* out) {
+  const int s = blockIdx.x;
+  if (threadIdx.x == 0) {
+    double acc = 0.0;
+    for (int k = 0; k < nb; ++k) acc += part[(size_t)s * nb + k];
+    out[s] = acc;
+  }
+}
+
+}  // namespace sre

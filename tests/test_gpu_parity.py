@@ -1,0 +1,186 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded inputs.
+
+Tolerances (reading C7): raw sums S_alpha relative 1e-10, M_alpha absolute
+1e-10, chi element-wise 1e-12 x max|chi|.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import sre_inputs as si
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def sre():
+    import paper_2601_07824_b200 as m
+    m.load()
+    return m
+
+
+def cuda(psi):
+    return torch.from_numpy(np.ascontiguousarray(psi)).to("cuda")
+
+
+def rel(a, b):
+    a, b = np.asarray(a, float), np.asarray(b, float)
+    return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300)))
+
+
+def gpu_sums(sre, psi, alphas, lo=None, hi=None):
+    t = cuda(psi)
+    n = t.shape[-1].bit_length() - 1
+    lo = 0 if lo is None else lo
+    hi = (1 << n) if hi is None else hi
+    out = sre.partial_sums(t, lo, hi, alphas)
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+ALPHAS = [0.5, 1.0, 1.5, 2.0, 3.0]
+
+
+@pytest.mark.parametrize("n", list(range(1, 15)))
+def test_full_sums_vs_oracle_all_paths(sre, oracle_lib, n):
+    """single-pass kernels (N <= 14): every raw sum vs Alg. 2 oracle, 5 alphas (two sweeps)."""
+    psi = si.haar(n, 1000 + n)
+    al = ALPHAS if n <= 12 else [1.0, 2.0, 3.0]
+    g = gpu_sums(sre, psi, al)[0]
+    o = oracle_lib.sums_fwht(psi, al)
+    assert rel(g[:-1], o[:-1]) < 1e-10
+    assert abs(g[-1] - o[-1]) <= 1e-10 * max(1.0, abs(o[-1]))
+
+
+@pytest.mark.parametrize("n", [15, 16, 17, 18, 19, 20, 21, 22, 23, 24, 25, 26])
+def test_two_pass_ranges_vs_oracle(sre, oracle_lib, n):
+    """two-pass path: sums over ragged X-string ranges (incl. a = 0 and unaligned ends) vs oracle."""
+    psi = si.haar(n, 2000 + n)
+    D = 1 << n
+    ranges = [(0, 3), (D - 5, D), (D // 2 + 7, D // 2 + 12)] if n >= 21 else [(0, 37), (D - 29, D), (D // 3, D // 3 + 41)]
+    al = [1.0, 2.0, 3.0] if n <= 20 else [2.0]
+    for lo, hi in ranges:
+        g = gpu_sums(sre, psi, al, lo, hi)[0]
+        o = oracle_lib.sums_fwht(psi, al, a_range=(lo, hi))
+        assert rel(g[:-1], o[:-1]) < 1e-10, (lo, hi)
+        if 1.0 in al:
+            assert abs(g[-1] - o[-1]) <= 1e-10 * abs(o[-1])
+
+
+@pytest.mark.parametrize("n", [1, 2, 5, 6, 10, 11, 13, 14, 15, 17, 20])
+def test_chi_elementwise(sre, oracle_lib, n):
+    """chi_b(a) for every b, sampled a, element by element against the oracle's Alg. 2 transform."""
+    psi = si.haar(n, 3000 + n)
+    D = 1 << n
+    rng = np.random.default_rng(n)
+    a_list = sorted({0, 1, D - 1, *[int(x) for x in rng.integers(0, D, 3)]})
+    t = cuda(psi)
+    for a in a_list:
+        g = sre.chi(t, a).cpu().numpy()
+        o = oracle_lib.chi(psi, a)
+        scale = max(np.max(np.abs(o)), 1e-300)
+        assert np.max(np.abs(g - o)) < 1e-12 * scale, a
+
+
+def test_config1_t_state_and_haar(sre, oracle_lib):
+    g = json.load(open(os.path.join(GOLD, "closed_forms.json")))
+    m, ln = sre.exact(cuda(si.t_state(8)), [1.0, 2.0, 3.0])
+    for mi, k in zip(m, ["1", "2", "3"]):
+        assert abs(mi - g["t_state_N8"][k]) < 1e-10
+    assert abs(ln) < 1e-12
+    psi = si.haar(8, 8001)
+    m, ln = sre.exact(cuda(psi), [2.0])
+    mo, lo = oracle_lib.sre(psi, [2.0], "brute")
+    assert abs(m[0] - mo[0]) < 1e-10 and abs(ln - lo) < 1e-12
+
+
+def test_paper_zero_state_bitwise(sre):
+    """P:1145-1146 printed SRE=-0.0 lost_norm=0.0 for |0>^16."""
+    gold = json.load(open(os.path.join(GOLD, "paper_zero_state.json")))
+    m, ln = sre.exact(cuda(si.zero(gold["N"])), [gold["alpha"]])
+    assert m[0] == 0.0 and math.copysign(1.0, m[0]) == -1.0
+    assert ln == 0.0
+
+
+def test_host_pointer_end_to_end(sre, oracle_lib):
+    psi = si.haar(11, 77)
+    m_host, _ = sre.exact(psi, [2.0, 3.0])          # numpy (host) -> copied inside the C call
+    m_dev, _ = sre.exact(cuda(psi), [2.0, 3.0])
+    assert m_host == m_dev
+    mo, _ = oracle_lib.sre(psi, [2.0, 3.0], "fwht")
+    assert max(abs(x - y) for x, y in zip(m_host, mo)) < 1e-10
+
+
+def test_stabilizer_and_t_doped(sre, oracle_lib):
+    for n in (6, 12, 16):
+        psi = si.random_clifford_state(n, 2 * n, 40 + n)
+        m, ln = sre.exact(cuda(psi), [1.0, 2.0, 3.0, 0.5])
+        assert max(abs(x) for x in m) < 1e-10 and abs(ln) < 1e-12
+    for t in (1, 3, 7):
+        psi = si.t_doped(15, t, 20, 90 + t)
+        m, _ = sre.exact(cuda(psi), [2.0, 3.0, 1.0])
+        for mi, a in zip(m, [2.0, 3.0, 1.0]):
+            assert abs(mi - oracle_lib.t_state_m(a, t)) < 1e-10
+
+
+def test_sharded_ranges_sum_to_full(sre):
+    """Sums over disjoint X-string shards add up to the single call (multi-GPU arithmetic)."""
+    for n in (9, 13, 16):
+        psi = si.haar(n, 555 + n)
+        D = 1 << n
+        full = gpu_sums(sre, psi, [2.0, 3.0])[0]
+        for G in (2, 4, 8):
+            parts = sum(gpu_sums(sre, psi, [2.0, 3.0], g * D // G, (g + 1) * D // G)[0] for g in range(G))
+            assert rel(parts[:-1], full[:-1]) < 1e-13
+
+
+def test_batched_config3_sampled(sre, oracle_lib):
+    """BASELINE config 3 shape (N=14 Clifford+T batch) on 16 states: T-doped closed forms on every
+    state of that kind, oracle ranges for the interleaved ones."""
+    batch, ts = si.config3_batch(14, 16, 14000)
+    idx = list(range(4)) + list(range(8, 12))
+    sub = batch[[i for i in range(16)]]
+    m, ln = sre.exact_batched(cuda(sub), [2.0])
+    for i in range(16):
+        assert abs(ln[i]) < 1e-10
+        if ts[i] is not None:
+            assert abs(m[i, 0] - oracle_lib.t_state_m(2.0, ts[i])) < 1e-10
+    g = sre.partial_sums(cuda(sub), 100, 164, [2.0]).cpu().numpy()
+    for i in idx:
+        o = oracle_lib.sums_fwht(sub[i], [2.0], a_range=(100, 164))
+        assert rel(g[i, :1], o[:1]) < 1e-10
+
+
+def test_scrambled_pair_n20(sre, oracle_lib):
+    """Exact pin for a generic entangled N=20 state: M(C(psi10 (x) phi10)) = M(psi10) + M(phi10)."""
+    lo, hi = si.haar(10, 2401), si.haar(10, 2402)
+    psi = si.scrambled_pair(lo, hi, 6, 2403)
+    m, ln = sre.exact(cuda(psi), [2.0])
+    ref = oracle_lib.sre(lo, [2.0])[0][0] + oracle_lib.sre(hi, [2.0])[0][0]
+    assert abs(m[0] - ref) < 1e-10
+    assert abs(ln) < 1e-10
+
+
+def test_error_paths(sre):
+    psi = cuda(si.haar(6, 1))
+    with pytest.raises(sre.SreError) as e:
+        sre.exact(psi * 1.01, [2.0])
+    assert e.value.code == 3
+    with pytest.raises(sre.SreError) as e:
+        sre.exact(psi, [0.0])
+    assert e.value.code == 1
+    with pytest.raises(sre.SreError) as e:
+        sre.exact(psi, [float("nan")])
+    assert e.value.code == 1
+    with pytest.raises(sre.SreError) as e:
+        sre.partial_sums(psi, 5, 3, [2.0])
+    assert e.value.code == 2
+    with pytest.raises(sre.SreError) as e:
+        sre.partial_sums(psi, 0, 65, [2.0])
+    assert e.value.code == 2
