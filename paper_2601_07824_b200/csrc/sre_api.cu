@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <atomic>
 #include <mutex>
@@ -114,7 +115,15 @@ struct Plan {
   int unitsA = 0, unitsB = 0, blkB = 0;
   size_t slab_doubles = 0;  // K * 2^N
   size_t slots = 0;         // partial slots per state
+  bool staged = false;      // L == 10: k_passA10s + k_passBp
+  int KG = 0;               // 8-X-string groups per staged launch
 };
+
+int staged_groups(int N) {
+  const char* e = getenv("SRE_KG");
+  if (e && atoi(e) > 0) return atoi(e) > 64 ? 64 : atoi(e);
+  return N >= 19 ? 2 : 8;  // N=20: 2 x 8 X-strings x 8 MiB = 128 MiB in flight
+}
 
 void two_pass_params(int T, int& L, int& H, int& CB) {
   L = T - 9;
@@ -166,6 +175,17 @@ int make_plan(int N, const Dev& d, Plan& p) {
     p.slab_doubles = (size_t)p.K << N;
     const uint64_t itemsB = (uint64_t)p.K * 2 * (1ull << (p.L - p.CB));
     p.slots = (size_t)((itemsB + p.unitsB - 1) / p.unitsB);
+    if (p.L == 10) {  // staged pass A + persistent pass B (N = 15..20)
+      p.staged = true;
+      p.KG = staged_groups(N);
+      if ((size_t)8 * p.KG > (size_t)p.K) {
+        p.K = 8 * p.KG;
+        p.slab_doubles = (size_t)p.K << N;
+        const uint64_t itemsK = (uint64_t)p.K * 2 * (1ull << (p.L - p.CB));  // generic pass B grid for K
+        p.slots = (size_t)((itemsK + p.unitsB - 1) / p.unitsB);
+      }
+      if (p.slots < 4 * 160) p.slots = 4 * 160;  // persistent grids: <= 4 CTAs x SMs
+    }
   }
   (void)d;
   return SRE_OK;
@@ -239,7 +259,7 @@ cudaError_t launch_small(int T, const double2* psi, int N, int B, int gx, uint64
   return cudaErrorInvalidValue;
 }
 
-constexpr int SMEM_128K = 2 * 32 * 256 * 8;
+constexpr int SMEM_128K = 2 * padded(32 * 256) * 8;  // 2 planes x (2^T + pad) x UPC units
 
 template <class K>
 cudaError_t set_smem(K kern, int bytes) {
@@ -303,7 +323,7 @@ template <int TP, int CB, bool A2, bool DBG>
 cudaError_t launch_passB_t(const Plan& p, uint64_t a0, int kcount, const double* ws, const Alphas& al, double* partial,
                            double* chi, cudaStream_t st) {
   constexpr int BLK = TP >= 14 ? 512 : 256;
-  constexpr int SM = BLK * 32 * 8;
+  constexpr int SM = padded(BLK * 32) * 8;
   static bool init = false;
   if (!init) {
     cudaError_t e = set_smem(k_passB<TP, CB, A2, DBG>, SM);
@@ -326,6 +346,67 @@ cudaError_t launch_passB(const Plan& p, uint64_t a0, int kcount, const double* w
 #define C_(tp, cb) case tp * 16 + cb: return launch_passB_t<tp, cb, A2, DBG>(p, a0, kcount, ws, al, partial, chi, st);
     C_(10, 6) C_(11, 6) C_(12, 6) C_(13, 6) C_(13, 5) C_(13, 4) C_(13, 3) C_(13, 2) C_(14, 2)
 #undef C_
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <int N>
+cudaError_t launch_passA10s_t(const Dev& d, const double2* psi, uint64_t a_first, int kcount, double* ws,
+                              cudaStream_t st) {
+  static bool init = false;
+  if (!init) {
+    cudaError_t e = set_smem(k_passA10s<N>, PA10_SMEM);
+    if (e != cudaSuccess) return e;
+    init = true;
+  }
+  const int groups = (kcount + 7) / 8;
+  const uint64_t items = (uint64_t)groups << (N - 11);
+  const unsigned grid = (unsigned)(items < (uint64_t)d.sms ? items : (uint64_t)d.sms);
+  return launch_counted(LK_PASSA, st, [&] {
+    k_passA10s<N><<<grid, 256, PA10_SMEM, st>>>(psi, a_first, kcount, groups, ws);
+    return cudaGetLastError();
+  });
+}
+
+cudaError_t launch_passA10s(const Plan& p, const Dev& d, const double2* psi, uint64_t a_first, int kcount,
+                            double* ws, cudaStream_t st) {
+  switch (p.N) {
+    case 15: return launch_passA10s_t<15>(d, psi, a_first, kcount, ws, st);
+    case 16: return launch_passA10s_t<16>(d, psi, a_first, kcount, ws, st);
+    case 17: return launch_passA10s_t<17>(d, psi, a_first, kcount, ws, st);
+    case 18: return launch_passA10s_t<18>(d, psi, a_first, kcount, ws, st);
+    case 19: return launch_passA10s_t<19>(d, psi, a_first, kcount, ws, st);
+    case 20: return launch_passA10s_t<20>(d, psi, a_first, kcount, ws, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <int CB, bool A2>
+cudaError_t launch_passBt_t(const Plan& p, const Dev& d, int kcount, const double* ws, const Alphas& al,
+                            double* partial, cudaStream_t st) {
+  static bool init = false;
+  if (!init) {
+    cudaError_t e = set_smem(k_passBt<CB, A2>, PBT_SMEM);
+    if (e != cudaSuccess) return e;
+    init = true;
+  }
+  const unsigned grid = (unsigned)d.sms;
+  return launch_counted(LK_PASSB, st, [&] {
+    k_passBt<CB, A2><<<grid, 256, PBT_SMEM, st>>>(p.N, kcount, ws, al, partial);
+    return cudaGetLastError();
+  });
+}
+
+template <bool A2>
+cudaError_t launch_passBp(const Plan& p, const Dev& d, int kcount, const double* ws, const Alphas& al, double* partial,
+                          cudaStream_t st) {
+  switch (12 - p.H) {  // slab-major tiles of 2^12 doubles: CB = 12 - H
+    case 8: return launch_passBt_t<8, A2>(p, d, kcount, ws, al, partial, st);
+    case 7: return launch_passBt_t<7, A2>(p, d, kcount, ws, al, partial, st);
+    case 6: return launch_passBt_t<6, A2>(p, d, kcount, ws, al, partial, st);
+    case 5: return launch_passBt_t<5, A2>(p, d, kcount, ws, al, partial, st);
+    case 4: return launch_passBt_t<4, A2>(p, d, kcount, ws, al, partial, st);
+    case 3: return launch_passBt_t<3, A2>(p, d, kcount, ws, al, partial, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -385,13 +466,37 @@ int run_range(const double2* psi, int N, int B, uint64_t a_begin, uint64_t a_end
       for (int s = 0; s < B; ++s) {
         const double2* ps = psi + ((size_t)s << N);
         CK(cudaMemsetAsync(partial, 0, sizeof(double) * p.slots * NACC, st));
-        for (uint64_t a = a_begin; a < a_end; a += (uint64_t)p.K) {
-          const int kc = (int)((a_end - a) < (uint64_t)p.K ? (a_end - a) : (uint64_t)p.K);
-          cudaError_t e = launch_passA(p, ps, a, kc, slab, st);
-          if (e != cudaSuccess) return fail(SRE_ECUDA, "passA: %s", cudaGetErrorString(e));
-          e = sw.a2 ? launch_passB<true, false>(p, a, kc, slab, sw.al, partial, nullptr, st)
-                    : launch_passB<false, false>(p, a, kc, slab, sw.al, partial, nullptr, st);
-          if (e != cudaSuccess) return fail(SRE_ECUDA, "passB: %s", cudaGetErrorString(e));
+        // generic batches (a < 2^L, unaligned heads, L > 10): k_passA + k_passB
+        auto generic = [&](uint64_t lo, uint64_t hi) -> int {
+          for (uint64_t a = lo; a < hi; a += (uint64_t)p.K) {
+            const int kc = (int)((hi - a) < (uint64_t)p.K ? (hi - a) : (uint64_t)p.K);
+            cudaError_t e = launch_passA(p, ps, a, kc, slab, st);
+            if (e != cudaSuccess) return fail(SRE_ECUDA, "passA: %s", cudaGetErrorString(e));
+            e = sw.a2 ? launch_passB<true, false>(p, a, kc, slab, sw.al, partial, nullptr, st)
+                      : launch_passB<false, false>(p, a, kc, slab, sw.al, partial, nullptr, st);
+            if (e != cudaSuccess) return fail(SRE_ECUDA, "passB: %s", cudaGetErrorString(e));
+          }
+          return SRE_OK;
+        };
+        if (!p.staged) {
+          int rc2 = generic(a_begin, a_end);
+          if (rc2) return rc2;
+        } else {
+          // staged groups need 8-aligned X-strings with a_h = a >> 10 != 0
+          uint64_t s0 = a_begin < 1024 ? 1024 : a_begin;
+          s0 = (s0 + 7) & ~7ull;
+          if (s0 > a_end) s0 = a_end;
+          int rc2 = generic(a_begin, s0);
+          if (rc2) return rc2;
+          const uint64_t per = (uint64_t)8 * p.KG;
+          for (uint64_t a = s0; a < a_end; a += per) {
+            const int kc = (int)((a_end - a) < per ? (a_end - a) : per);
+            cudaError_t e = launch_passA10s(p, d, ps, a, kc, slab, st);
+            if (e != cudaSuccess) return fail(SRE_ECUDA, "passA10s: %s", cudaGetErrorString(e));
+            e = sw.a2 ? launch_passBp<true>(p, d, kc, slab, sw.al, partial, st)
+                      : launch_passBp<false>(p, d, kc, slab, sw.al, partial, st);
+            if (e != cudaSuccess) return fail(SRE_ECUDA, "passBp: %s", cudaGetErrorString(e));
+          }
         }
         ra.nslots = (int)p.slots;
         CK(launch_counted(LK_AUX, st, [&] {

@@ -15,7 +15,8 @@
 // Transform engine: a "unit" of NT = 2^(T-5) threads holds a 2^T-point real vector, 32 values
 // per thread.  Round k puts 5 index bits [s_k, s_k+5) in the register index j (radix-32
 // butterflies in registers); between rounds the unit transposes through shared memory with
-// the XOR swizzle swz(e) = e ^ ((e >> 5) & 15) (conflict-free for every round layout).
+// one pad double per 32 (swz(e) = e + (e >> 5): additive addressing, conflict-free for every
+// round layout).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -44,7 +45,10 @@ __device__ __forceinline__ uint64_t ins0(uint64_t y, int p) {  // insert a 0 bit
 __device__ __forceinline__ uint32_t lay(uint32_t t, uint32_t j, int s) {
   return (t & ((1u << s) - 1u)) | (j << s) | ((t >> s) << (s + 5));
 }
-__device__ __forceinline__ uint32_t swz(uint32_t e) { return e ^ ((e >> 5) & 15u); }
+// shared-memory index of element e: one pad double per 32 (additive, conflict-free for every
+// round layout because the half-warp's lanes always span 4 distinct bits of e)
+__device__ __forceinline__ uint32_t swz(uint32_t e) { return e + (e >> 5); }
+__host__ __device__ constexpr int padded(int n) { return n + n / 32; }
 
 struct Round { int s, rlo, rhi; };
 __host__ __device__ constexpr int nrounds(int T, int LO) {
@@ -90,28 +94,41 @@ struct BarCta { __device__ __forceinline__ void sync() const { __syncthreads(); 
 // Rounds K..end of the transform of NP planes (each a 2^T vector in its own 2^T smem slice).
 // On entry the registers hold round K-1's layout (or round 0's with butterflies pending if
 // K == 0); on exit the final round's layout with all butterflies done.
-template <int T, int LO, int K, int NP, class Bar>
+template <int T, int LO, int K, int NP, class Bar, bool SEQ = false>
 struct Rounds {
+  // SEQ: the NP planes share one 2^T smem slice and are exchanged one after the other.
   __device__ __forceinline__ static void run(double (&v)[NP][32], double* sm, uint32_t t, const Bar& bar) {
     constexpr int NR = nrounds(T, LO);
     if constexpr (K < NR) {
       constexpr Round r = round_k(T, LO, K);
       if constexpr (K > 0) {
         constexpr Round q = round_k(T, LO, K - 1);
-        bar.sync();
+        if constexpr (SEQ) {
 #pragma unroll
-        for (int pl = 0; pl < NP; ++pl)
+          for (int pl = 0; pl < NP; ++pl) {
+            bar.sync();
 #pragma unroll
-          for (int j = 0; j < 32; ++j) sm[pl * (1 << T) + swz(lay(t, j, q.s))] = v[pl][j];
-        bar.sync();
+            for (int j = 0; j < 32; ++j) sm[swz(lay(t, j, q.s))] = v[pl][j];
+            bar.sync();
 #pragma unroll
-        for (int pl = 0; pl < NP; ++pl)
+            for (int j = 0; j < 32; ++j) v[pl][j] = sm[swz(lay(t, j, r.s))];
+          }
+        } else {
+          bar.sync();
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[pl][j] = sm[pl * (1 << T) + swz(lay(t, j, r.s))];
+          for (int pl = 0; pl < NP; ++pl)
+#pragma unroll
+            for (int j = 0; j < 32; ++j) sm[pl * padded(1 << T) + swz(lay(t, j, q.s))] = v[pl][j];
+          bar.sync();
+#pragma unroll
+          for (int pl = 0; pl < NP; ++pl)
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[pl][j] = sm[pl * padded(1 << T) + swz(lay(t, j, r.s))];
+        }
       }
 #pragma unroll
       for (int pl = 0; pl < NP; ++pl) bfly32<r.rlo, r.rhi>(v[pl]);
-      Rounds<T, LO, K + 1, NP, Bar>::run(v, sm, t, bar);
+      Rounds<T, LO, K + 1, NP, Bar, SEQ>::run(v, sm, t, bar);
     }
   }
 };
@@ -297,7 +314,7 @@ __global__ void __launch_bounds__(256, 1) k_mid(const double2* __restrict__ psi_
   const double2* psi = psi_all + ((size_t)blockIdx.y << N);
   const uint32_t t = threadIdx.x & (NT - 1);
   const int unit = threadIdx.x / NT;
-  double* sm = smem + (size_t)unit * 2 * (1 << T);
+  double* sm = smem + (size_t)unit * 2 * padded(1 << T);
   double acc[NACC];
 #pragma unroll
   for (int i = 0; i < NACC; ++i) acc[i] = 0.0;
@@ -336,7 +353,7 @@ __global__ void __launch_bounds__(256, 1) k_passA(const double2* __restrict__ ps
   const int H = N - 1 - L;
   const uint32_t t = threadIdx.x & (NT - 1);
   const int unit = threadIdx.x / NT;
-  double* sm = smem + (size_t)unit * 2 * (1 << L);
+  double* sm = smem + (size_t)unit * 2 * padded(1 << L);
   const uint64_t item = (uint64_t)blockIdx.x * UPC + unit;  // item = k * 2^H + y_h
   const uint64_t rows = 1ull << H;
   if (item >= (uint64_t)kcount * rows) return;  // whole units only; bars are per unit
@@ -369,7 +386,7 @@ __global__ void __launch_bounds__(TP >= 14 ? 512 : 256, 1) k_passB(int N, int L,
   extern __shared__ double smem[];
   const uint32_t t = threadIdx.x & (NT - 1);
   const int unit = threadIdx.x / NT;
-  double* sm = smem + (size_t)unit * (1 << TP);
+  double* sm = smem + (size_t)unit * padded(1 << TP);
   double acc[NACC];
 #pragma unroll
   for (int i = 0; i < NACC; ++i) acc[i] = 0.0;
@@ -407,6 +424,190 @@ __global__ void __launch_bounds__(TP >= 14 ? 512 : 256, 1) k_passB(int N, int L,
   }
   (void)H;
   if constexpr (!DEBUG) block_flush(acc, partial, blockIdx.x);
+}
+
+// ------------------------------------------------------------------------------------------
+// Staged pass A for L = 10 (N = 15..20): a persistent CTA of 8 warps walks the rows y_h of a
+// group of up to 8 X-strings that share a_h = a >> 10 (hence the pivot p >= 10 and the two
+// psi rows x_h = ins0(y_h, p-10), x_h ^ a_h).  The two rows (2 x 16 KB) are staged in shared
+// memory with cp.async, double-buffered one row ahead; warp w generates X-string a0 + w from
+// the staged rows (q = row[y_l], r = partner_row[y_l ^ a_l]), transforms 10 bits with one
+// warp-local exchange, and writes its row of both planes.  Items = (group, row).
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int NPEND>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(NPEND) : "memory"); }
+
+// mbarrier / bulk-copy (TMA) helpers
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n.reg .pred P;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+      "@!P bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(b)) : "memory");
+}
+
+constexpr int PA10_NS = 4;                                   // staging ring depth
+constexpr int PA10_SMEM = PA10_NS * 2 * 1024 * 16 + 8 * padded(1024) * 8;  // 128 KB ring + 66 KB exchange
+
+// Staged pass A for L = 10 (N = 15..20).  A persistent CTA of 8 warps walks items
+// (group g of 8 X-strings sharing a_h != 0, row y_h).  The two psi rows an item needs
+// (x_h = ins0(y_h, p-10) and x_h ^ a_h, 16 KB each) arrive by two bulk copies into a 4-deep
+// ring completed on an mbarrier; warps run free (no CTA barrier): the last of the 8 warps to
+// finish with a ring slot refills it with the item NS positions ahead.  Warp w generates
+// X-string 8g + w from the staged rows, transforms 10 bits (one warp-local exchange per
+// plane) and writes its row of both planes.
+template <int N>
+__global__ void __launch_bounds__(256, 1) k_passA10s(const double2* __restrict__ psi, uint64_t a_first,
+                                                     int kcount, int groups, double* __restrict__ ws) {
+  constexpr int cb = 12 - (N - 11);                             // pass B tile = 2^12 doubles
+  extern __shared__ __align__(128) double smem[];
+  double2* ring = reinterpret_cast<double2*>(smem);             // [NS][q row | r row][1024]
+  double* exch = smem + PA10_NS * 2 * 1024 * 2;                 // [warp][padded 1024]
+  __shared__ __align__(8) uint64_t full[PA10_NS];
+  __shared__ int used[PA10_NS];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int H = N - 11;
+  constexpr uint64_t rows = 1ull << H;
+  const uint64_t items = rows * (uint64_t)groups;
+  constexpr size_t plane = (size_t)1 << (N - 1);
+  auto issue = [&](uint64_t item, int slot) {                  // one thread
+    const uint64_t g = item >> H, yh = item & (rows - 1);
+    const uint64_t ag = a_first + 8 * g;
+    const int p = 63 - __clzll((long long)ag);
+    const uint64_t xh = ins0(yh, p - 10);
+    double2* dst = ring + (size_t)slot * 2048;
+    mbar_expect_tx(&full[slot], 2 * 1024 * 16);
+    bulk_g2s(dst, psi + (xh << 10), 1024 * 16, &full[slot]);
+    bulk_g2s(dst + 1024, psi + ((xh ^ (ag >> 10)) << 10), 1024 * 16, &full[slot]);
+  };
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < PA10_NS; ++i) { mbar_init(&full[i], 1); used[i] = 0; }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int i = 0; i < PA10_NS; ++i)
+      if (blockIdx.x + (uint64_t)i * gridDim.x < items) issue(blockIdx.x + (uint64_t)i * gridDim.x, i);
+  double* xw = exch + (size_t)w * padded(1024);
+  uint32_t n = 0;
+  for (uint64_t item = blockIdx.x; item < items; item += gridDim.x, ++n) {
+    const int slot = (int)(n % PA10_NS);
+    mbar_wait(&full[slot], (n / PA10_NS) & 1u);
+    const uint64_t g = item >> H, yh = item & (rows - 1);
+    const int k = 8 * (int)g + w;
+    const double2* sq = ring + (size_t)slot * 2048;
+    double v[2][32];
+    const bool active = k < kcount;
+    if (active) {
+      const uint32_t al = (uint32_t)((a_first + (uint64_t)k) & 1023u);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const uint32_t yl = lane + 32 * j;
+        const double2 q = sq[yl];
+        const double2 r = sq[1024 + (yl ^ al)];
+        v[0][j] = fma(r.x, q.x, r.y * q.y);
+        v[1][j] = fma(r.x, q.y, -(r.y * q.x));
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {                                             // release the slot; last warp refills
+      const int prev = atomicAdd(&used[slot], 1);
+      if (prev == 7) {
+        atomicExch(&used[slot], 0);
+        const uint64_t nx = item + (uint64_t)PA10_NS * gridDim.x;
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        if (nx < items) issue(nx, slot);
+      }
+    }
+    if (active) {
+      Rounds<10, 0, 0, 2, BarWarp, true>::run(v, xw, lane, BarWarp{});
+      // slab-major workspace: (y_h, pos) -> ((pos >> cb) << (H + cb)) | (y_h << cb) | (pos & (C-1))
+      double* w0 = ws + (size_t)k * 2 * plane + (yh << cb);
+      constexpr uint32_t cm = (1u << cb) - 1u;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const uint32_t pos = lane + 32 * j;
+        const size_t off = ((size_t)(pos >> cb) << (H + cb)) + (pos & cm);   // compile-time in j
+        __stcg(w0 + off, v[0][j]);
+        __stcg(w0 + plane + off, v[1][j]);
+      }
+    }
+  }
+}
+
+// Pass B over the slab-major workspace written by k_passA10s: a tile (X-string k, plane, slab)
+// is one contiguous block of 2^TP doubles (2^H rows x C = 2^CB columns).  A CTA holds two
+// independent 128-thread units (TP = 12); each streams its tiles through a 3-deep ring of bulk
+// copies completed on mbarriers, reads the tile in the round-0 layout, and uses the same slot
+// for its shared-memory exchange before handing it back to the copy engine.
+constexpr int PBT_NS = 3;
+constexpr int PBT_SLOT = padded(4096);          // 32 KB tile + exchange padding
+constexpr int PBT_SMEM = 2 * PBT_NS * PBT_SLOT * 8;   // 2 units x 3 slots x 33 KB
+
+template <int CB, bool A2>
+__global__ void __launch_bounds__(256, 1) k_passBt(int N, int kcount, const double* __restrict__ ws, Alphas al,
+                                                   double* partial) {
+  constexpr int TP = 12, NT = 128, UNITS = 2, TILE = 1 << TP;
+  extern __shared__ __align__(128) double smem[];
+  __shared__ __align__(8) uint64_t full[UNITS][PBT_NS];
+  const int unit = threadIdx.x / NT;
+  const uint32_t t = threadIdx.x % NT;
+  const int L = N - 1 - (TP - CB);
+  const uint64_t slabs = 1ull << (L - CB);
+  const uint64_t tiles = (uint64_t)kcount * 2 * slabs;   // tile = kp * slabs + slab, contiguous blocks
+  double* ring = smem + (size_t)unit * PBT_NS * PBT_SLOT;
+  const BarNamed bar{1 + unit, NT};
+  if (threadIdx.x == 0) {
+    for (int u = 0; u < UNITS; ++u)
+      for (int i = 0; i < PBT_NS; ++i) mbar_init(&full[u][i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const uint64_t first = (uint64_t)blockIdx.x * UNITS + unit, step = (uint64_t)gridDim.x * UNITS;
+  auto issue = [&](uint64_t tile, int slot) {
+    mbar_expect_tx(&full[unit][slot], TILE * 8);
+    bulk_g2s(ring + (size_t)slot * PBT_SLOT, ws + tile * TILE, TILE * 8, &full[unit][slot]);
+  };
+  if (t == 0)
+    for (int i = 0; i < PBT_NS; ++i)
+      if (first + i * step < tiles) issue(first + i * step, i);
+  double acc[NACC];
+#pragma unroll
+  for (int i = 0; i < NACC; ++i) acc[i] = 0.0;
+  uint32_t n = 0;
+  for (uint64_t tile = first; tile < tiles; tile += step, ++n) {
+    const int slot = (int)(n % PBT_NS);
+    double* buf = ring + (size_t)slot * PBT_SLOT;
+    mbar_wait(&full[unit][slot], (n / PBT_NS) & 1u);
+    double v[1][32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[0][j] = buf[t + NT * j];   // round-0 layout e = t + NT j
+    Rounds<TP, CB, 0, 1, BarNamed>::run(v, buf, t, bar);
+    bar.sync();                                                  // slot free: refill it
+    if (t == 0) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      const uint64_t nx = tile + (uint64_t)PBT_NS * step;
+      if (nx < tiles) issue(nx, slot);
+    }
+#pragma unroll
+    for (int j = 0; j < 32; ++j) Epi<A2>::add(acc, v[0][j], al);
+  }
+  block_flush(acc, partial, blockIdx.x);
 }
 
 // ------------------------------------------------------------------------------------------
