@@ -185,7 +185,8 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     label, n, b, alphas, seed = CONFIGS[args.config]
     D = 1 << n
-    lo, hi = rank * D // world, (rank + 1) * D // world   # contiguous X-string shard
+    from paper_2601_07824_b200.dist import shard_range
+    lo, hi = shard_range(n, rank, world)                 # contiguous X-string shard
     psi_host = make_state(args.config)
     psi = torch.from_numpy(psi_host).to(dev)            # replicated on every GPU (same seed)
     ws = torch.empty(sre.workspace_size(n, b, len(alphas)), dtype=torch.uint8, device=dev)

@@ -125,10 +125,11 @@ int sre_chi(const void* psi, int N, uint64_t a, double* chi_dev, void* stream);
  *   sre_launch_count   : cumulative number of kernels this library launched in the process.
  *   sre_profile_begin  : start sampling; every stride-th launch of each kernel kind is bracketed
  *                        by CUDA events on its own stream.
- *   sre_profile_end    : stop; per kind k (0 single-pass, 1 pass A, 2 pass B, 3 auxiliary)
+ *   sre_profile_end    : stop; per kind k (0 single-pass, 1 pass A, 2 pass B, 3 auxiliary,
+ *                        4 fused persistent two-pass)
  *                        ms_sum[k] = summed event time of the sampled launches, n_timed[k] = how
  *                        many were sampled, n_launched[k] = launches of that kind since begin.
- *                        Arrays have 4 entries each (any may be NULL).  Synchronises the events.
+ *                        Arrays have 5 entries each (any may be NULL).  Synchronises the events.
  */
 uint64_t sre_launch_count(void);
 int sre_profile_begin(int stride);

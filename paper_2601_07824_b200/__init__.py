@@ -203,7 +203,7 @@ def chi(psi, a: int):
     return torch.view_as_complex(out.view(-1, 2))
 
 
-KINDS = ("single_pass", "pass_a", "pass_b", "aux")
+KINDS = ("single_pass", "pass_a", "pass_b", "aux", "fused")
 
 
 def launch_count() -> int:
@@ -219,8 +219,8 @@ def profile_begin(stride: int = 1) -> None:
 def profile_end() -> dict:
     """{kind: {"ms_sum", "timed", "launched"}} for the launches since profile_begin()."""
     lib = load()
-    ms = np.zeros(4)
-    nt = (ctypes.c_uint64 * 4)()
-    nl = (ctypes.c_uint64 * 4)()
+    ms = np.zeros(len(KINDS))
+    nt = (ctypes.c_uint64 * len(KINDS))()
+    nl = (ctypes.c_uint64 * len(KINDS))()
     _check(lib.sre_profile_end(_dp(ms), nt, nl))
     return {k: {"ms_sum": float(ms[i]), "timed": int(nt[i]), "launched": int(nl[i])} for i, k in enumerate(KINDS)}

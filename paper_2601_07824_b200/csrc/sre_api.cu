@@ -38,13 +38,13 @@ int fail(int code, const char* fmt, ...) {
 // ------------------------------------------------------------------------------------------
 // launch accounting and sampled per-kernel timing (bench.py's roofline numbers)
 // ------------------------------------------------------------------------------------------
-enum LaunchKind { LK_SINGLE = 0, LK_PASSA = 1, LK_PASSB = 2, LK_AUX = 3, LK_N = 4 };
+enum LaunchKind { LK_SINGLE = 0, LK_PASSA = 1, LK_PASSB = 2, LK_AUX = 3, LK_FUSED = 4, LK_N = 5 };
 
 struct Prof {
   std::mutex mu;
   bool on = false;
   int stride = 1;
-  uint64_t launched[LK_N] = {0, 0, 0, 0};
+  uint64_t launched[LK_N] = {0, 0, 0, 0, 0};
   std::vector<cudaEvent_t> pool;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed[LK_N];
 };
@@ -194,7 +194,13 @@ int make_plan(int N, const Dev& d, Plan& p) {
 size_t ws_bytes_for(const Plan& p, int B) {
   size_t partial = p.slots * NACC * (p.kind == TWOPASS ? 1 : (size_t)B);
   size_t norm = 4096 * (size_t)B + (size_t)B;
-  return (partial + p.slab_doubles + norm) * sizeof(double) + 256;
+  return (partial + p.slab_doubles + norm + 64) * sizeof(double) + 256;   // + FusedCtl
+}
+// FusedCtl lives after the norm area
+FusedCtl* ctl_of(char* ws, const Plan& p, int B) {
+  size_t partial = p.slots * NACC * (p.kind == TWOPASS ? 1 : (size_t)B);
+  size_t norm = 4096 * (size_t)B + (size_t)B;
+  return reinterpret_cast<FusedCtl*>(reinterpret_cast<double*>(ws) + partial + p.slab_doubles + norm);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -381,6 +387,39 @@ cudaError_t launch_passA10s(const Plan& p, const Dev& d, const double2* psi, uin
   return cudaErrorInvalidValue;
 }
 
+bool fused_enabled() {  // opt-in (SRE_FUSED=1): measured slower than the two staged launches
+  const char* e = getenv("SRE_FUSED");
+  return e && e[0] == '1';
+}
+
+template <int N, bool A2>
+cudaError_t launch_fused_t(const Dev& d, const double2* psi, uint64_t a_first, uint64_t count, double* ws,
+                           FusedCtl* ctl, const Alphas& al, double* partial, cudaStream_t st) {
+  static bool init = false;
+  if (!init) {
+    cudaError_t e = set_smem(k_fused<N, A2>, FZ_SMEM);
+    if (e != cudaSuccess) return e;
+    init = true;
+  }
+  cudaError_t e = cudaMemsetAsync(ctl, 0, sizeof(FusedCtl), st);
+  if (e != cudaSuccess) return e;
+  return launch_counted(LK_FUSED, st, [&] {
+    void* args[] = {(void*)&psi, (void*)&a_first, (void*)&count, (void*)&ws, (void*)&ctl, (void*)&al, (void*)&partial};
+    return cudaLaunchCooperativeKernel((const void*)k_fused<N, A2>, dim3(d.sms), dim3(256), args, FZ_SMEM, st);
+  });
+}
+
+template <bool A2>
+cudaError_t launch_fused(const Plan& p, const Dev& d, const double2* psi, uint64_t a_first, uint64_t count,
+                         double* ws, FusedCtl* ctl, const Alphas& al, double* partial, cudaStream_t st) {
+  switch (p.N) {
+#define C_(n) case n: return launch_fused_t<n, A2>(d, psi, a_first, count, ws, ctl, al, partial, st);
+    C_(15) C_(16) C_(17) C_(18) C_(19) C_(20)
+#undef C_
+  }
+  return cudaErrorInvalidValue;
+}
+
 template <int CB, bool A2>
 cudaError_t launch_passBt_t(const Plan& p, const Dev& d, int kcount, const double* ws, const Alphas& al,
                             double* partial, cudaStream_t st) {
@@ -430,6 +469,8 @@ int run_range(const double2* psi, int N, int B, uint64_t a_begin, uint64_t a_end
   double* partial = reinterpret_cast<double*>(ws);
   const size_t partial_doubles = p.slots * NACC * (p.kind == TWOPASS ? 1 : (size_t)B);
   double* slab = partial + partial_doubles;
+  FusedCtl* ctl = ctl_of(ws, p, B);
+  CK(cudaMemsetAsync(ctl, 0, sizeof(FusedCtl), st));
   const uint64_t count = a_end - a_begin;
   CK(cudaMemsetAsync(sums_dev, 0, sizeof(double) * (size_t)B * (n_alpha + 2), st));
   if (count == 0) return SRE_OK;
@@ -442,6 +483,7 @@ int run_range(const double2* psi, int N, int B, uint64_t a_begin, uint64_t a_end
     ra.n_this = sw.al.n;
     ra.write_common = sw.first == 0;
     for (int i = 0; i < MAXA; ++i) ra.scale4[i] = sw.scale4[i];
+    ra.err = &ctl->error;
     if (p.kind == SMALL || p.kind == MID) {
       int gx;
       if (p.kind == SMALL) {
@@ -488,6 +530,12 @@ int run_range(const double2* psi, int N, int B, uint64_t a_begin, uint64_t a_end
           if (s0 > a_end) s0 = a_end;
           int rc2 = generic(a_begin, s0);
           if (rc2) return rc2;
+          if (fused_enabled() && s0 < a_end) {   // one persistent launch for the aligned bulk
+            cudaError_t e = sw.a2 ? launch_fused<true>(p, d, ps, s0, a_end - s0, slab, ctl, sw.al, partial, st)
+                                  : launch_fused<false>(p, d, ps, s0, a_end - s0, slab, ctl, sw.al, partial, st);
+            if (e != cudaSuccess) return fail(SRE_ECUDA, "fused: %s", cudaGetErrorString(e));
+            s0 = a_end;
+          }
           const uint64_t per = (uint64_t)8 * p.KG;
           for (uint64_t a = s0; a < a_end; a += per) {
             const int kc = (int)((a_end - a) < per ? (a_end - a) : per);

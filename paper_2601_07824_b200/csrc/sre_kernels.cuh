@@ -163,6 +163,19 @@ struct Epi {
   }
 };
 
+// Epilogue of one tile's 32 values per thread into a fresh local sum, then one add into the
+// long-lived accumulators: keeps the running-sum chains ~32x shorter (DESIGN "Summation").
+template <bool A2>
+__device__ __forceinline__ void tile_accumulate(double (&acc)[NACC], const double (&v)[32], const Alphas& al) {
+  double loc[NACC];
+#pragma unroll
+  for (int i = 0; i < NACC; ++i) loc[i] = 0.0;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) Epi<A2>::add(loc, v[j], al);
+#pragma unroll
+  for (int i = 0; i < NACC; ++i) acc[i] += loc[i];
+}
+
 // Block reduction of the NACC accumulators; thread 0 adds them to partial[slot].
 __device__ __forceinline__ void block_flush(double (&acc)[NACC], double* partial, int slot) {
   __shared__ double red[32][NACC];
@@ -332,8 +345,8 @@ __global__ void __launch_bounds__(256, 1) k_mid(const double2* __restrict__ psi_
         chi_store(chi, a, p, 1, lay(t, j, sf), v[1][j]);
       }
     } else {
-#pragma unroll
-      for (int j = 0; j < 32; ++j) { Epi<A2>::add(acc, v[0][j], al); Epi<A2>::add(acc, v[1][j], al); }
+      tile_accumulate<A2>(acc, v[0], al);
+      tile_accumulate<A2>(acc, v[1], al);
     }
   }
   if constexpr (!DEBUG) block_flush(acc, partial, blockIdx.y * gridDim.x + blockIdx.x);
@@ -418,8 +431,7 @@ __global__ void __launch_bounds__(TP >= 14 ? 512 : 256, 1) k_passB(int N, int L,
         chi_store(chi, a, p, pl, (bh << L) | bl, v[0][j]);
       }
     } else {
-#pragma unroll
-      for (int j = 0; j < 32; ++j) Epi<A2>::add(acc, v[0][j], al);
+      tile_accumulate<A2>(acc, v[0], al);
     }
   }
   (void)H;
@@ -604,10 +616,246 @@ __global__ void __launch_bounds__(256, 1) k_passBt(int N, int kcount, const doub
       const uint64_t nx = tile + (uint64_t)PBT_NS * step;
       if (nx < tiles) issue(nx, slot);
     }
-#pragma unroll
-    for (int j = 0; j < 32; ++j) Epi<A2>::add(acc, v[0][j], al);
+    tile_accumulate<A2>(acc, v[0], al);
   }
   block_flush(acc, partial, blockIdx.x);
+}
+
+// ------------------------------------------------------------------------------------------
+// k_fused: the whole two-pass sweep for N = 15..20 in ONE persistent launch (grid = #SMs,
+// cooperative so every CTA is resident).  Each CTA runs two roles concurrently:
+//   warps 0-3 ("A"): items (batch b, row y_h); a batch is 4 consecutive X-strings sharing a_h;
+//                    the two psi rows arrive by bulk copy in a ring shared by the 4 warps;
+//                    warp w generates X-string 4b + w and transforms the 10 low bits
+//                    (same arithmetic as k_passA10s), writing the slab-major workspace slot b%S.
+//   warps 4-7 ("B"): one 128-thread unit; tiles (batch b, plane, slab) of 2^12 doubles arrive by
+//                    bulk copy (same arithmetic as k_passBt) and go through the H row bits and
+//                    the epilogue.
+// Work comes from two global tickets (in order), and the only waits are on earlier work:
+//   A-item of batch b waits until every B-tile of batch b - S has been copied in (slot reuse);
+//   B-tile of batch b waits until every A-item of batch b has been written.
+// Waits spin on L2 counters with acquire loads and a 10 s watchdog that records an error.
+// ------------------------------------------------------------------------------------------
+struct FusedCtl {              // zeroed by the host before each launch
+  unsigned long long a_next, b_next;
+  unsigned long long a_done[4], b_done[4];
+  int error;
+};
+constexpr int FZ_S = 2;                      // workspace slots (batches in flight)
+constexpr int FZ_KB = 4;                     // X-strings per batch (= A warps)
+constexpr int FZ_NSA = 3;                    // A staging ring depth (32 KB each)
+constexpr int FZ_NSB = 2;                    // B tile ring depth (33 KB each)
+constexpr int FZ_SMEM = FZ_NSA * 2048 * 16 + FZ_KB * padded(1024) * 8 + FZ_NSB * padded(4096) * 8;
+
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_add(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.release.gpu.global.add.u64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;\n" : "=l"(t));
+  return t;
+}
+// spin until *p >= target; false (and ctl->error set) on a 10 s timeout
+__device__ __forceinline__ bool wait_geq(const unsigned long long* p, unsigned long long target, FusedCtl* ctl) {
+  if (ld_acquire(p) >= target) return true;
+  const uint64_t t0 = gtimer();
+  while (ld_acquire(p) < target) {
+    __nanosleep(200);
+    if (gtimer() - t0 > 10000000000ull || *(volatile int*)&ctl->error) { atomicExch(&ctl->error, 1); return false; }
+  }
+  return true;
+}
+
+template <int N, bool A2>
+__global__ void __launch_bounds__(256, 1) k_fused(const double2* __restrict__ psi, uint64_t a_first, uint64_t count,
+                                                  double* __restrict__ ws, FusedCtl* ctl, Alphas al, double* partial) {
+  constexpr int H = N - 11, CB = 12 - H, TP = 12, TILE = 1 << TP;
+  constexpr uint64_t ROWS = 1ull << H;
+  constexpr uint64_t SLABS = 1ull << (10 - CB);
+  constexpr uint64_t TPB = (uint64_t)FZ_KB * 2 * SLABS;   // B tiles per full batch
+  constexpr size_t PLANE = (size_t)1 << (N - 1);
+  constexpr size_t SLOT = (size_t)FZ_KB * 2 * PLANE;     // doubles per workspace slot
+  constexpr uint64_t END = ~0ull;
+  extern __shared__ __align__(128) double smem[];
+  double2* ringA = reinterpret_cast<double2*>(smem);                          // [NSA][2048]
+  double* exA = smem + FZ_NSA * 2048 * 2;                                     // [4][padded 1024]
+  double* ringB = exA + FZ_KB * padded(1024);                                 // [NSB][padded 4096]
+  __shared__ __align__(8) uint64_t fullA[FZ_NSA], fullB[FZ_NSB];
+  __shared__ uint64_t itemA[FZ_NSA], itemB[FZ_NSB];
+  __shared__ int usedA[FZ_NSA];
+  __shared__ double redB[4][NACC];
+  const uint64_t nbatch = (count + FZ_KB - 1) / FZ_KB;
+  const uint64_t totA = nbatch * ROWS;
+  const uint64_t totB = (count / FZ_KB) * TPB + (count % FZ_KB) * 2 * SLABS;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < FZ_NSA; ++i) { mbar_init(&fullA[i], 1); usedA[i] = 0; }
+    for (int i = 0; i < FZ_NSB; ++i) mbar_init(&fullB[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  // A producer (one thread, never waits): next A ticket into ring slot s, stage its psi rows
+  auto produceA = [&](int s) {
+    const uint64_t t = atomicAdd(&ctl->a_next, 1ull);
+    if (t >= totA) {
+      itemA[s] = END;
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&fullA[s])) : "memory");
+      return;
+    }
+    const uint64_t b = t >> H, yh = t & (ROWS - 1);
+    const uint64_t ag = a_first + FZ_KB * b;
+    const int p = 63 - __clzll((long long)ag);
+    const uint64_t xh = ins0(yh, p - 10);
+    itemA[s] = t;
+    double2* dst = ringA + (size_t)s * 2048;
+    mbar_expect_tx(&fullA[s], 2 * 1024 * 16);
+    bulk_g2s(dst, psi + (xh << 10), 1024 * 16, &fullA[s]);
+    bulk_g2s(dst + 1024, psi + ((xh ^ (ag >> 10)) << 10), 1024 * 16, &fullA[s]);
+  };
+
+  if (w < 4) {
+    // ======================= A role =======================
+    if (threadIdx.x == 0)
+      for (int s = 0; s < FZ_NSA; ++s) produceA(s);
+    double* xw = exA + (size_t)w * padded(1024);
+    for (uint32_t n = 0;; ++n) {
+      const int s = (int)(n % FZ_NSA);
+      mbar_wait(&fullA[s], (n / FZ_NSA) & 1u);
+      const uint64_t t = itemA[s];
+      if (t == END) break;
+      const uint64_t b = t >> H, yh = t & (ROWS - 1);
+      const uint64_t kglob = FZ_KB * b + w;
+      const bool active = kglob < count;
+      double v[2][32];
+      if (active) {
+        const uint32_t alow = (uint32_t)((a_first + kglob) & 1023u);
+        const double2* sq = ringA + (size_t)s * 2048;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const uint32_t yl = lane + 32 * j;
+          const double2 q = sq[yl];
+          const double2 r = sq[1024 + (yl ^ alow)];
+          v[0][j] = fma(r.x, q.x, r.y * q.y);
+          v[1][j] = fma(r.x, q.y, -(r.y * q.x));
+        }
+        Rounds<10, 0, 0, 2, BarWarp, true>::run(v, xw, lane, BarWarp{});
+        // workspace slot b%S is free once every B tile of batch b - S has been copied out
+        if (b >= FZ_S && lane == 0) wait_geq(&ctl->b_done[b % FZ_S], (b / FZ_S) * TPB, ctl);
+        __syncwarp();
+        double* w0 = ws + (b % FZ_S) * SLOT + (size_t)w * 2 * PLANE + (yh << CB);
+        constexpr uint32_t cm = (1u << CB) - 1u;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const uint32_t pos = lane + 32 * j;
+          const size_t off = ((size_t)(pos >> CB) << (H + CB)) + (pos & cm);
+          __stcg(w0 + off, v[0][j]);
+          __stcg(w0 + PLANE + off, v[1][j]);
+        }
+        __threadfence();
+      }
+      __syncwarp();
+      if (lane == 0) {
+        // the last of the 4 warps to finish this item publishes it and refills the ring slot
+        if (atomicAdd(&usedA[s], 1) == FZ_KB - 1) {
+          atomicExch(&usedA[s], 0);
+          __threadfence();
+          red_release_add(&ctl->a_done[b % FZ_S], 1ull);
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          produceA(s);
+        }
+      }
+    }
+  } else {
+    // ======================= B role =======================
+    const uint32_t tb = threadIdx.x - 128;
+    const BarNamed bar{1, 128};
+    double acc[NACC];
+#pragma unroll
+    for (int i = 0; i < NACC; ++i) acc[i] = 0.0;
+    // Leader-only producer state.  positions [0, issued) are staged; [0, credited) have been
+    // credited to b_done (their copy has landed, so the workspace slot no longer needs them).
+    // A claimed tile may have to wait for its batch; before the leader waits it credits every
+    // staged position, so nothing another warp waits on is ever held back by that wait.
+    uint32_t issued = 0, credited = 0;
+    bool ended = false;
+    auto credit_upto = [&](uint32_t upto) {
+      for (; credited < upto; ++credited) {
+        const int cs = (int)(credited % FZ_NSB);
+        mbar_wait(&fullB[cs], (credited / FZ_NSB) & 1u);
+        const uint64_t ct = itemB[cs];
+        if (ct != END) red_release_add(&ctl->b_done[(ct / TPB) % FZ_S], 1ull);
+      }
+    };
+    auto produce_upto = [&](uint32_t upto) {     // fill positions [issued, upto)
+      while (issued < upto && !ended) {
+        const int ps = (int)(issued % FZ_NSB);
+        const uint64_t t = atomicAdd(&ctl->b_next, 1ull);
+        if (t >= totB) {
+          itemB[ps] = END;
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&fullB[ps])) : "memory");
+          ++issued;
+          ended = true;
+          return;
+        }
+        const uint64_t b = t / TPB;
+        const unsigned long long need = (b / FZ_S + 1) * ROWS;
+        if (ld_acquire(&ctl->a_done[b % FZ_S]) < need) {
+          credit_upto(issued);
+          if (!wait_geq(&ctl->a_done[b % FZ_S], need, ctl)) {
+            itemB[ps] = END;
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&fullB[ps])) : "memory");
+            ++issued;
+            ended = true;
+            return;
+          }
+        }
+        asm volatile("fence.proxy.async.global;\n" ::: "memory");
+        itemB[ps] = t;
+        mbar_expect_tx(&fullB[ps], TILE * 8);
+        bulk_g2s(ringB + (size_t)ps * padded(TILE), ws + (b % FZ_S) * SLOT + (t % TPB) * TILE, TILE * 8, &fullB[ps]);
+        ++issued;
+      }
+    };
+    for (uint32_t n = 0;; ++n) {
+      const int s = (int)(n % FZ_NSB);
+      if (tb == 0) {
+        produce_upto(n + FZ_NSB);
+        credit_upto(n + 1);                      // this position's copy has landed
+      }
+      mbar_wait(&fullB[s], (n / FZ_NSB) & 1u);
+      const uint64_t t = itemB[s];
+      if (t == END) break;
+      double* buf = ringB + (size_t)s * padded(TILE);
+      double v[1][32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[0][j] = buf[tb + 128 * j];
+      Rounds<TP, CB, 0, 1, BarNamed>::run(v, buf, tb, bar);
+      bar.sync();                                // the slot's smem is free for the next copy
+      if (tb == 0) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      tile_accumulate<A2>(acc, v[0], al);
+    }
+    // B-role accumulators -> partial[blockIdx.x]
+#pragma unroll
+    for (int i = 0; i < NACC; ++i) {
+      double x = acc[i];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      if (lane == 0) redB[w - 4][i] = x;
+    }
+    bar.sync();
+    if (tb < NACC) {
+      double sacc = 0.0;
+      for (int k = 0; k < 4; ++k) sacc += redB[k][tb];
+      partial[(size_t)blockIdx.x * NACC + tb] += sacc;
+    }
+  }
 }
 
 // ------------------------------------------------------------------------------------------
@@ -621,6 +869,7 @@ struct ReduceArgs {
   int n_this;       // alphas in this sweep
   int write_common; // 1: also write purity and t ln t (sweep 0)
   double scale4[MAXA];  // 4^alpha_i
+  const int* err;   // nonzero => a persistent kernel's watchdog fired: results are NaN
 };
 __global__ void k_reduce(const double* __restrict__ partial, ReduceArgs r, double* out) {
   // one block (one warp) per state; column sums over slots in fixed order
@@ -636,6 +885,10 @@ __global__ void k_reduce(const double* __restrict__ partial, ReduceArgs r, doubl
   __syncwarp();
   if (i == 0) {
     double* o = out + (size_t)s * (r.n_alpha + 2);
+    if (r.err && *r.err) {
+      for (int k = 0; k < r.n_alpha + 2; ++k) o[k] = __longlong_as_double(0x7ff8000000000000ll);
+      return;
+    }
     for (int k = 0; k < r.n_this; ++k) o[r.first + k] = col[k] * r.scale4[k];
     if (r.write_common) {
       o[r.n_alpha] = 4.0 * col[MAXA];

@@ -1,0 +1,79 @@
+"""N>1 host path on CPU: world_size-2 gloo process group, shards computed by the oracle, one
+all_reduce, finalised by the library's host-side sre_finalize (no GPU needed)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import sre_inputs as si
+
+torch = pytest.importorskip("torch")
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, n, alphas, out_q):
+    import torch.distributed as dist
+
+    import oracle
+    import paper_2601_07824_b200 as sre
+    from paper_2601_07824_b200 import dist as sdist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    psi = si.haar(n, 777)
+
+    def part(lo, hi):
+        return torch.from_numpy(oracle.sums_fwht(psi, alphas, a_range=(lo, hi))).reshape(1, -1)
+
+    def allreduce(t):
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+
+    m, ln = sdist.exact_sharded(n, alphas, rank, world, part, allreduce, lambda s: sre.finalize(s.numpy(), n, alphas))
+    out_q.put((rank, m.tolist(), float(ln[0])))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_sharded_equals_single(world):
+    import torch.multiprocessing as mp
+
+    import oracle
+    oracle.build()
+    n, alphas = 9, [1.0, 2.0, 3.0]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, alphas, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ref_m, ref_ln = oracle.sre(si.haar(n, 777), alphas, "fwht")
+    for _, m, ln in res:
+        assert np.max(np.abs(np.array(m[0]) - np.array(ref_m))) < 1e-12
+        assert abs(ln - ref_ln) < 1e-13
+
+
+def test_shard_plan_partitions():
+    from paper_2601_07824_b200.dist import shard_range
+    for n in (1, 3, 10, 20):
+        for world in (1, 2, 3, 4, 5, 8):
+            if world > (1 << n):
+                continue
+            rs = [shard_range(n, r, world) for r in range(world)]
+            assert rs[0][0] == 0 and rs[-1][1] == 1 << n
+            assert all(rs[i][1] == rs[i + 1][0] for i in range(world - 1))
+            sizes = [b - a for a, b in rs]
+            assert max(sizes) - min(sizes) <= 1

@@ -184,3 +184,35 @@ def test_error_paths(sre):
     with pytest.raises(sre.SreError) as e:
         sre.partial_sums(psi, 0, 65, [2.0])
     assert e.value.code == 2
+
+
+def test_config2_full_vs_frozen_oracle(sre):
+    """BASELINE config 2 (N=16 Haar, alpha in {1,2,3}) in full against the oracle's frozen sums
+    (tests/golden/oracle_c2.json, written by tools/make_fixtures.py from oracle/ only)."""
+    import hashlib
+    g = json.load(open(os.path.join(GOLD, "oracle_c2.json")))
+    psi = si.haar(g["n"], g["seed"])
+    assert hashlib.sha256(psi.tobytes()).hexdigest() == g["psi_sha256"]
+    s = gpu_sums(sre, psi, g["alphas"])[0]
+    assert rel(s[:-1], g["sums"][:-1]) < 1e-10
+    assert abs(s[-1] - g["sums"][-1]) <= 1e-10 * abs(g["sums"][-1])
+    m, ln = sre.exact(cuda(psi), g["alphas"])
+    assert max(abs(a - b) for a, b in zip(m, g["M"])) < 1e-10
+    assert abs(ln) < 1e-10
+
+
+def test_config5_n24_sampled_and_t_state(sre, oracle_lib):
+    """BASELINE config 5 size (N=24): sampled X-string ranges vs the oracle, and |T>^24 per
+    X-string closed form (product state: S_a = prod_j s_j(a_j) with s(0) = 1 + 0, s(1) = 2 (1/2)^alpha)."""
+    n = 24
+    psi = si.haar(n, 24001)
+    for lo, hi in ((123456, 123460), ((1 << 24) - 3, 1 << 24)):
+        g = gpu_sums(sre, psi, [2.0], lo, hi)[0]
+        o = oracle_lib.sums_fwht(psi, [2.0], a_range=(lo, hi))
+        assert rel(g[:2], o[:2]) < 1e-10
+    t = si.t_state(n)
+    for a in (0, 1, 0xABCDE, (1 << 24) - 1):
+        g = gpu_sums(sre, t, [2.0], a, a + 1)[0]
+        w = bin(a).count("1")
+        expect = (1.0 ** 2) ** (n - w) * (2 * 0.5 ** 2.0) ** w   # <I>,<Z>: (1, 0); <X>,<Y>: 1/sqrt2 each
+        assert abs(g[0] - expect) <= 1e-12 * expect

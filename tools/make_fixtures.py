@@ -1,7 +1,7 @@
 """Freeze full-size oracle values as JSON fixtures (calls only oracle/ and sre_inputs/).
 
     python tools/make_fixtures.py c2      # N=16 Haar seed 16001, alpha in {1,2,3}   (minutes)
-    python tools/make_fixtures.py c4      # N=20 Haar seed 20001, alpha = 2           (~1 h, 8 cores)
+    python tools/make_fixtures.py c4      # N=20 Haar seed 20001, alpha = 2  (~15 h on 8 cores: not frozen)
 
 Each fixture records the input recipe and the SHA-256 of the state's bytes, so a test can
 regenerate the identical state and compare the CUDA path with the frozen oracle sums.
