@@ -116,8 +116,15 @@ struct Plan {
   size_t slab_doubles = 0;  // K * 2^N
   size_t slots = 0;         // partial slots per state
   bool staged = false;      // L == 10: k_passA10s + k_passBp
+  bool tmem = false;        // N = 19, 20: TMEM pass B (H = 8) + k_passA11t / k_passA10s<RM>
+  uint64_t amin = 0;        // first X-string the staged / TMEM kernels accept (a_h != 0)
   int KG = 0;               // 8-X-string groups per staged launch
 };
+
+bool tmem_enabled() {  // opt-in (SRE_TMEM=1): the 4-warp TMEM pass B measured slower (37 vs 30 us)
+  const char* e = getenv("SRE_TMEM");
+  return e && e[0] == '1';
+}
 
 int staged_groups(int N) {
   const char* e = getenv("SRE_KG");
@@ -129,6 +136,8 @@ void two_pass_params(int T, int& L, int& H, int& CB) {
   L = T - 9;
   if (L < 10) L = 10;
   if (L > 13) L = 13;
+  if (T >= 20 && T <= 23) L = 12;   // streamed path (N = 21..24): two 128-thread units per CTA
+  if (T == 24) L = 13;              // N = 25: one 256-thread unit (keeps pass-B rows >= 32 B)
   H = T - L;
   CB = 13 - H;
   if (CB > 6) CB = 6;
@@ -166,7 +175,7 @@ int make_plan(int N, const Dev& d, Plan& p) {
     two_pass_params(p.T, p.L, p.H, p.CB);
     p.TP = p.CB + p.H;
     uint64_t k = (1ull << 23) >> N;  // K * 2^N doubles ~ 64 MiB of workspace in flight
-    if (k < 2) k = 2;
+    if (k < 8) k = 8;                 // N >= 21: HBM workspace; 8 X-strings share each psi row pair
     if (k > 64) k = 64;
     p.K = (int)k;
     p.unitsA = 256 >> (p.L - 5);
@@ -175,6 +184,12 @@ int make_plan(int N, const Dev& d, Plan& p) {
     p.slab_doubles = (size_t)p.K << N;
     const uint64_t itemsB = (uint64_t)p.K * 2 * (1ull << (p.L - p.CB));
     p.slots = (size_t)((itemsB + p.unitsB - 1) / p.unitsB);
+    if (N >= 21 && N <= 25) {  // streamed pass A (k_passAs) + TMA-fed pass B with 2^13-double tiles
+      p.staged = true;
+      p.KG = 1;
+      p.amin = 1ull << p.L;
+      if (p.slots < 4 * 160) p.slots = 4 * 160;
+    }
     if (p.L == 10) {  // staged pass A + persistent pass B (N = 15..20)
       p.staged = true;
       p.KG = staged_groups(N);
@@ -185,6 +200,11 @@ int make_plan(int N, const Dev& d, Plan& p) {
         p.slots = (size_t)((itemsK + p.unitsB - 1) / p.unitsB);
       }
       if (p.slots < 4 * 160) p.slots = 4 * 160;  // persistent grids: <= 4 CTAs x SMs
+      p.amin = 1024;
+    }
+    if ((N == 19 || N == 20) && tmem_enabled()) {
+      p.tmem = true;
+      p.amin = N == 20 ? 2048 : 1024;
     }
   }
   (void)d;
@@ -374,9 +394,83 @@ cudaError_t launch_passA10s_t(const Dev& d, const double2* psi, uint64_t a_first
   });
 }
 
+template <int N>
+cudaError_t launch_passA_tmem_t(const Dev& d, const double2* psi, uint64_t a_first, int kcount, double* ws,
+                                cudaStream_t st) {
+  constexpr int L = N == 20 ? 11 : 10;
+  constexpr int SMEM = N == 20 ? PA11_SMEM : PA10_SMEM;
+  auto kern = [] { if constexpr (N == 20) return k_passA11t<20>; else return k_passA10s<N, true>; }();
+  static bool init = false;
+  if (!init) {
+    cudaError_t e = set_smem(kern, SMEM);
+    if (e != cudaSuccess) return e;
+    init = true;
+  }
+  const int groups = (kcount + 7) / 8;
+  const uint64_t items = (uint64_t)groups << (N - 1 - L);
+  const unsigned grid = (unsigned)(items < (uint64_t)d.sms ? items : (uint64_t)d.sms);
+  return launch_counted(LK_PASSA, st, [&] {
+    kern<<<grid, 256, SMEM, st>>>(psi, a_first, kcount, groups, ws);
+    return cudaGetLastError();
+  });
+}
+
+template <int N, bool A2>
+cudaError_t launch_passB_tmem_t(const Dev& d, int kcount, const double* ws, const Alphas& al, double* partial,
+                                cudaStream_t st) {
+  static bool init = false;
+  if (!init) {
+    cudaError_t e = set_smem(k_passBt8<N, A2>, PB8_SMEM);
+    if (e != cudaSuccess) return e;
+    init = true;
+  }
+  return launch_counted(LK_PASSB, st, [&] {
+    k_passBt8<N, A2><<<d.sms, 128, PB8_SMEM, st>>>(kcount, ws, al, partial);
+    return cudaGetLastError();
+  });
+}
+
+cudaError_t launch_tmem_pair(const Plan& p, const Dev& d, bool a2, const double2* psi, uint64_t a_first, int kcount,
+                             double* ws, const Alphas& al, double* partial, cudaStream_t st) {
+  cudaError_t e;
+  if (p.N == 20) {
+    e = launch_passA_tmem_t<20>(d, psi, a_first, kcount, ws, st);
+    if (e == cudaSuccess) e = a2 ? launch_passB_tmem_t<20, true>(d, kcount, ws, al, partial, st)
+                                 : launch_passB_tmem_t<20, false>(d, kcount, ws, al, partial, st);
+  } else {
+    e = launch_passA_tmem_t<19>(d, psi, a_first, kcount, ws, st);
+    if (e == cudaSuccess) e = a2 ? launch_passB_tmem_t<19, true>(d, kcount, ws, al, partial, st)
+                                 : launch_passB_tmem_t<19, false>(d, kcount, ws, al, partial, st);
+  }
+  return e;
+}
+
+template <int N, int L>
+cudaError_t launch_passAs_t(const Dev& d, const double2* psi, uint64_t a_first, int kcount, double* ws,
+                            cudaStream_t st) {
+  static bool init = false;
+  if (!init) {
+    cudaError_t e = set_smem(k_passAs<N, L>, pas_smem(L));
+    if (e != cudaSuccess) return e;
+    init = true;
+  }
+  const uint64_t units = (uint64_t)kcount << (N - 1 - L);
+  const uint64_t ctas = (units + (256 >> (L - 5)) - 1) / (256 >> (L - 5));
+  const unsigned grid = (unsigned)(ctas < (uint64_t)d.sms ? ctas : (uint64_t)d.sms);
+  return launch_counted(LK_PASSA, st, [&] {
+    k_passAs<N, L><<<grid, 256, pas_smem(L), st>>>(psi, a_first, kcount, ws);
+    return cudaGetLastError();
+  });
+}
+
 cudaError_t launch_passA10s(const Plan& p, const Dev& d, const double2* psi, uint64_t a_first, int kcount,
                             double* ws, cudaStream_t st) {
   switch (p.N) {
+    case 21: return launch_passAs_t<21, 12>(d, psi, a_first, kcount, ws, st);
+    case 22: return launch_passAs_t<22, 12>(d, psi, a_first, kcount, ws, st);
+    case 23: return launch_passAs_t<23, 12>(d, psi, a_first, kcount, ws, st);
+    case 24: return launch_passAs_t<24, 12>(d, psi, a_first, kcount, ws, st);
+    case 25: return launch_passAs_t<25, 13>(d, psi, a_first, kcount, ws, st);
     case 15: return launch_passA10s_t<15>(d, psi, a_first, kcount, ws, st);
     case 16: return launch_passA10s_t<16>(d, psi, a_first, kcount, ws, st);
     case 17: return launch_passA10s_t<17>(d, psi, a_first, kcount, ws, st);
@@ -420,18 +514,18 @@ cudaError_t launch_fused(const Plan& p, const Dev& d, const double2* psi, uint64
   return cudaErrorInvalidValue;
 }
 
-template <int CB, bool A2>
+template <int TP, int CB, bool A2>
 cudaError_t launch_passBt_t(const Plan& p, const Dev& d, int kcount, const double* ws, const Alphas& al,
                             double* partial, cudaStream_t st) {
   static bool init = false;
   if (!init) {
-    cudaError_t e = set_smem(k_passBt<CB, A2>, PBT_SMEM);
+    cudaError_t e = set_smem(k_passBt<TP, CB, A2>, pbt_smem(TP));
     if (e != cudaSuccess) return e;
     init = true;
   }
   const unsigned grid = (unsigned)d.sms;
   return launch_counted(LK_PASSB, st, [&] {
-    k_passBt<CB, A2><<<grid, 256, PBT_SMEM, st>>>(p.N, kcount, ws, al, partial);
+    k_passBt<TP, CB, A2><<<grid, 256, pbt_smem(TP), st>>>(p.N, kcount, ws, al, partial);
     return cudaGetLastError();
   });
 }
@@ -439,13 +533,24 @@ cudaError_t launch_passBt_t(const Plan& p, const Dev& d, int kcount, const doubl
 template <bool A2>
 cudaError_t launch_passBp(const Plan& p, const Dev& d, int kcount, const double* ws, const Alphas& al, double* partial,
                           cudaStream_t st) {
+  if (p.N >= 21) {     // streamed path: tiles of 2^13 doubles, CB = 13 - H
+    switch (13 - p.H) {
+      case 7: return launch_passBt_t<13, 7, A2>(p, d, kcount, ws, al, partial, st);
+      case 6: return launch_passBt_t<13, 6, A2>(p, d, kcount, ws, al, partial, st);
+      case 5: return launch_passBt_t<13, 5, A2>(p, d, kcount, ws, al, partial, st);
+      case 4: return launch_passBt_t<13, 4, A2>(p, d, kcount, ws, al, partial, st);
+      case 3: return launch_passBt_t<13, 3, A2>(p, d, kcount, ws, al, partial, st);
+      case 2: return launch_passBt_t<13, 2, A2>(p, d, kcount, ws, al, partial, st);
+    }
+    return cudaErrorInvalidValue;
+  }
   switch (12 - p.H) {  // slab-major tiles of 2^12 doubles: CB = 12 - H
-    case 8: return launch_passBt_t<8, A2>(p, d, kcount, ws, al, partial, st);
-    case 7: return launch_passBt_t<7, A2>(p, d, kcount, ws, al, partial, st);
-    case 6: return launch_passBt_t<6, A2>(p, d, kcount, ws, al, partial, st);
-    case 5: return launch_passBt_t<5, A2>(p, d, kcount, ws, al, partial, st);
-    case 4: return launch_passBt_t<4, A2>(p, d, kcount, ws, al, partial, st);
-    case 3: return launch_passBt_t<3, A2>(p, d, kcount, ws, al, partial, st);
+    case 8: return launch_passBt_t<12, 8, A2>(p, d, kcount, ws, al, partial, st);
+    case 7: return launch_passBt_t<12, 7, A2>(p, d, kcount, ws, al, partial, st);
+    case 6: return launch_passBt_t<12, 6, A2>(p, d, kcount, ws, al, partial, st);
+    case 5: return launch_passBt_t<12, 5, A2>(p, d, kcount, ws, al, partial, st);
+    case 4: return launch_passBt_t<12, 4, A2>(p, d, kcount, ws, al, partial, st);
+    case 3: return launch_passBt_t<12, 3, A2>(p, d, kcount, ws, al, partial, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -503,7 +608,7 @@ int run_range(const double2* psi, int N, int B, uint64_t a_begin, uint64_t a_end
                   : launch_mid<false, false>(p.T, psi, N, B, gx, a_begin, count, sw.al, partial, nullptr, st);
       if (e != cudaSuccess) return fail(SRE_ECUDA, "launch: %s", cudaGetErrorString(e));
       ra.nslots = gx;
-      CK(launch_counted(LK_AUX, st, [&] { k_reduce<<<B, 32, 0, st>>>(partial, ra, sums_dev); return cudaGetLastError(); }));
+      CK(launch_counted(LK_AUX, st, [&] { k_reduce<<<B, 256, 0, st>>>(partial, ra, sums_dev); return cudaGetLastError(); }));
     } else {
       for (int s = 0; s < B; ++s) {
         const double2* ps = psi + ((size_t)s << N);
@@ -524,19 +629,27 @@ int run_range(const double2* psi, int N, int B, uint64_t a_begin, uint64_t a_end
           int rc2 = generic(a_begin, a_end);
           if (rc2) return rc2;
         } else {
-          // staged groups need 8-aligned X-strings with a_h = a >> 10 != 0
-          uint64_t s0 = a_begin < 1024 ? 1024 : a_begin;
+          // staged groups need 8-aligned X-strings with a_h = a >> L != 0
+          uint64_t s0 = a_begin < p.amin ? p.amin : a_begin;
           s0 = (s0 + 7) & ~7ull;
           if (s0 > a_end) s0 = a_end;
           int rc2 = generic(a_begin, s0);
           if (rc2) return rc2;
-          if (fused_enabled() && s0 < a_end) {   // one persistent launch for the aligned bulk
+          if (fused_enabled() && p.L == 10 && s0 < a_end) {   // one persistent launch for the aligned bulk
             cudaError_t e = sw.a2 ? launch_fused<true>(p, d, ps, s0, a_end - s0, slab, ctl, sw.al, partial, st)
                                   : launch_fused<false>(p, d, ps, s0, a_end - s0, slab, ctl, sw.al, partial, st);
             if (e != cudaSuccess) return fail(SRE_ECUDA, "fused: %s", cudaGetErrorString(e));
             s0 = a_end;
           }
           const uint64_t per = (uint64_t)8 * p.KG;
+          if (p.tmem) {
+            for (uint64_t a = s0; a < a_end; a += per) {
+              const int kc = (int)((a_end - a) < per ? (a_end - a) : per);
+              cudaError_t e = launch_tmem_pair(p, d, sw.a2, ps, a, kc, slab, sw.al, partial, st);
+              if (e != cudaSuccess) return fail(SRE_ECUDA, "tmem pair: %s", cudaGetErrorString(e));
+            }
+            s0 = a_end;
+          }
           for (uint64_t a = s0; a < a_end; a += per) {
             const int kc = (int)((a_end - a) < per ? (a_end - a) : per);
             cudaError_t e = launch_passA10s(p, d, ps, a, kc, slab, st);
@@ -548,7 +661,7 @@ int run_range(const double2* psi, int N, int B, uint64_t a_begin, uint64_t a_end
         }
         ra.nslots = (int)p.slots;
         CK(launch_counted(LK_AUX, st, [&] {
-          k_reduce<<<1, 32, 0, st>>>(partial, ra, sums_dev + (size_t)s * (n_alpha + 2));
+          k_reduce<<<1, 256, 0, st>>>(partial, ra, sums_dev + (size_t)s * (n_alpha + 2));
           return cudaGetLastError();
         }));
       }

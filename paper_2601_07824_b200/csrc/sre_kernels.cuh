@@ -22,6 +22,8 @@
 #include <cuda_runtime.h>
 #include <type_traits>
 
+#include "tmem.cuh"
+
 namespace sre {
 
 constexpr int MAXA = 4;          // Renyi indices per sweep (more are done in extra sweeps)
@@ -367,11 +369,13 @@ __global__ void __launch_bounds__(256, 1) k_passA(const double2* __restrict__ ps
   const uint32_t t = threadIdx.x & (NT - 1);
   const int unit = threadIdx.x / NT;
   double* sm = smem + (size_t)unit * 2 * padded(1 << L);
-  const uint64_t item = (uint64_t)blockIdx.x * UPC + unit;  // item = k * 2^H + y_h
+  // item = y_h * kcount + k: the X-strings of the batch (which share a_h) take the same psi rows
+  // at the same time, so each row pair comes from HBM once per batch and from L2 otherwise
+  const uint64_t item = (uint64_t)blockIdx.x * UPC + unit;
   const uint64_t rows = 1ull << H;
   if (item >= (uint64_t)kcount * rows) return;  // whole units only; bars are per unit
-  const int k = (int)(item >> H);
-  const uint64_t yh = item & (rows - 1);
+  const int k = (int)(item % (uint64_t)kcount);
+  const uint64_t yh = item / (uint64_t)kcount;
   const uint64_t a = a0 + (uint64_t)k;
   const int p = pivot_of(a, N);
   double v[2][32];
@@ -446,6 +450,15 @@ __global__ void __launch_bounds__(TP >= 14 ? 512 : 256, 1) k_passB(int N, int L,
 // the staged rows (q = row[y_l], r = partner_row[y_l ^ a_l]), transforms 10 bits with one
 // warp-local exchange, and writes its row of both planes.  Items = (group, row).
 // ------------------------------------------------------------------------------------------
+// Chunk-major workspace for the TMEM pass B (H = 8): within a plane, position group
+// g = pos >> 7 (128 positions), then chunk c = y_h & 7, then m = y_h >> 3, then pos & 127.
+// A pass-B chunk (rows {c + 8m}, one 128-position group) is one contiguous 32 KB block.
+__device__ __forceinline__ size_t cm_row_off(uint64_t yh) { return (size_t)(((yh & 7) << 5) | (yh >> 3)) << 7; }
+template <int J>   // offset of position lane + 32 J (+ 1024 h) minus the lane: compile time
+__device__ __forceinline__ constexpr size_t cm_pos_off(int h) {
+  return ((size_t)((J >> 2) + 8 * h) << 15) + 32 * (J & 3);
+}
+
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gsrc) : "memory");
@@ -483,10 +496,10 @@ constexpr int PA10_SMEM = PA10_NS * 2 * 1024 * 16 + 8 * padded(1024) * 8;  // 12
 // finish with a ring slot refills it with the item NS positions ahead.  Warp w generates
 // X-string 8g + w from the staged rows, transforms 10 bits (one warp-local exchange per
 // plane) and writes its row of both planes.
-template <int N>
+template <int N, bool RM = false>   // RM: row-major workspace for the TMEM pass B (pos = lane + 32 j)
 __global__ void __launch_bounds__(256, 1) k_passA10s(const double2* __restrict__ psi, uint64_t a_first,
                                                      int kcount, int groups, double* __restrict__ ws) {
-  constexpr int cb = 12 - (N - 11);                             // pass B tile = 2^12 doubles
+  constexpr int cb = RM ? 10 : 12 - (N - 11);                   // pass B tile = 2^12 doubles
   extern __shared__ __align__(128) double smem[];
   double2* ring = reinterpret_cast<double2*>(smem);             // [NS][q row | r row][1024]
   double* exch = smem + PA10_NS * 2 * 1024 * 2;                 // [warp][padded 1024]
@@ -548,7 +561,19 @@ __global__ void __launch_bounds__(256, 1) k_passA10s(const double2* __restrict__
     }
     if (active) {
       Rounds<10, 0, 0, 2, BarWarp, true>::run(v, xw, lane, BarWarp{});
-      // slab-major workspace: (y_h, pos) -> ((pos >> cb) << (H + cb)) | (y_h << cb) | (pos & (C-1))
+      // slab-major workspace: (y_h, pos) -> ((pos >> cb) << (H + cb)) | (y_h << cb) | (pos & (C-1));
+      // RM (TMEM pass B, H = 8): chunk-major ((pos >> 7) << 15) + row_off(y_h) + (pos & 127)
+      if constexpr (RM) {
+        static_assert(H == 8, "chunk-major layout assumes H = 8");
+        double* w1 = ws + (size_t)k * 2 * plane + cm_row_off(yh) + lane;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const size_t o = ((size_t)(j >> 2) << 15) + 32 * (j & 3);
+          __stcg(w1 + o, v[0][j]);
+          __stcg(w1 + plane + o, v[1][j]);
+        }
+        continue;
+      }
       double* w0 = ws + (size_t)k * 2 * plane + (yh << cb);
       constexpr uint32_t cm = (1u << cb) - 1u;
 #pragma unroll
@@ -568,13 +593,13 @@ __global__ void __launch_bounds__(256, 1) k_passA10s(const double2* __restrict__
 // copies completed on mbarriers, reads the tile in the round-0 layout, and uses the same slot
 // for its shared-memory exchange before handing it back to the copy engine.
 constexpr int PBT_NS = 3;
-constexpr int PBT_SLOT = padded(4096);          // 32 KB tile + exchange padding
-constexpr int PBT_SMEM = 2 * PBT_NS * PBT_SLOT * 8;   // 2 units x 3 slots x 33 KB
+__host__ __device__ constexpr int pbt_slot(int TP) { return padded(1 << TP); }         // tile + exchange padding
+__host__ __device__ constexpr int pbt_smem(int TP) { return PBT_NS * 256 / (1 << (TP - 5)) * pbt_slot(TP) * 8; }
 
-template <int CB, bool A2>
+template <int TP, int CB, bool A2>   // TP = 12: two 128-thread units; TP = 13: one 256-thread unit
 __global__ void __launch_bounds__(256, 1) k_passBt(int N, int kcount, const double* __restrict__ ws, Alphas al,
                                                    double* partial) {
-  constexpr int TP = 12, NT = 128, UNITS = 2, TILE = 1 << TP;
+  constexpr int NT = 1 << (TP - 5), UNITS = 256 / NT, TILE = 1 << TP, SLOT = pbt_slot(TP);
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t full[UNITS][PBT_NS];
   const int unit = threadIdx.x / NT;
@@ -582,7 +607,7 @@ __global__ void __launch_bounds__(256, 1) k_passBt(int N, int kcount, const doub
   const int L = N - 1 - (TP - CB);
   const uint64_t slabs = 1ull << (L - CB);
   const uint64_t tiles = (uint64_t)kcount * 2 * slabs;   // tile = kp * slabs + slab, contiguous blocks
-  double* ring = smem + (size_t)unit * PBT_NS * PBT_SLOT;
+  double* ring = smem + (size_t)unit * PBT_NS * SLOT;
   const BarNamed bar{1 + unit, NT};
   if (threadIdx.x == 0) {
     for (int u = 0; u < UNITS; ++u)
@@ -593,7 +618,7 @@ __global__ void __launch_bounds__(256, 1) k_passBt(int N, int kcount, const doub
   const uint64_t first = (uint64_t)blockIdx.x * UNITS + unit, step = (uint64_t)gridDim.x * UNITS;
   auto issue = [&](uint64_t tile, int slot) {
     mbar_expect_tx(&full[unit][slot], TILE * 8);
-    bulk_g2s(ring + (size_t)slot * PBT_SLOT, ws + tile * TILE, TILE * 8, &full[unit][slot]);
+    bulk_g2s(ring + (size_t)slot * SLOT, ws + tile * TILE, TILE * 8, &full[unit][slot]);
   };
   if (t == 0)
     for (int i = 0; i < PBT_NS; ++i)
@@ -604,7 +629,7 @@ __global__ void __launch_bounds__(256, 1) k_passBt(int N, int kcount, const doub
   uint32_t n = 0;
   for (uint64_t tile = first; tile < tiles; tile += step, ++n) {
     const int slot = (int)(n % PBT_NS);
-    double* buf = ring + (size_t)slot * PBT_SLOT;
+    double* buf = ring + (size_t)slot * SLOT;
     mbar_wait(&full[unit][slot], (n / PBT_NS) & 1u);
     double v[1][32];
 #pragma unroll
@@ -619,6 +644,113 @@ __global__ void __launch_bounds__(256, 1) k_passBt(int N, int kcount, const doub
     tile_accumulate<A2>(acc, v[0], al);
   }
   block_flush(acc, partial, blockIdx.x);
+}
+
+// ------------------------------------------------------------------------------------------
+// Streamed pass A for L = 12, 13 (N = 21..25): persistent units of 2^(L-5) threads walk items
+// (row y_h, X-string k) in row-major order, so the K X-strings of a launch read the same psi
+// rows back to back (HBM once, L2 for the rest).  Generation operands stream as 32 chunks of
+// 2^(L-5) y values (q chunk + r chunk, the r chunk index permuted by a_l >> (L-5)) through an
+// 8-deep bulk-copy ring per unit; then three rounds (two unit-wide exchanges, one plane at a
+// time) and a slab-major store for the TMA-fed pass B (tile = 2^13 doubles, CB = 13 - H).
+// L = 12 runs two independent 128-thread units per CTA so one unit's exchange barriers overlap
+// the other's arithmetic (L = 13's single CTA-wide unit measured barrier-bound).
+// ------------------------------------------------------------------------------------------
+constexpr int PAS_NS = 2;   // ring stages per unit
+constexpr int PAS_JS = 8;   // j-blocks per stage: copies of 8 x 2^(L-5) complex (16 KB at L = 12)
+__host__ __device__ constexpr int pas_smem(int L) {
+  // per unit: ring of NS stages x (q | r) x JS*NT complex  +  one padded plane of 2^L doubles
+  return (256 >> (L - 5)) * (PAS_NS * 2 * PAS_JS * (1 << (L - 5)) * 16 + padded(1 << L) * 8);
+}
+
+template <int N, int L>
+__global__ void __launch_bounds__(256, 1) k_passAs(const double2* __restrict__ psi, uint64_t a_first, int kcount,
+                                                   double* __restrict__ ws) {
+  constexpr int NT = 1 << (L - 5), UNITS = 256 / NT, WPU = NT / 32;   // threads, units, warps per unit
+  constexpr int H = N - 1 - L, CB = 13 - H;                            // pass-B tile = 2^13 doubles
+  constexpr int SPI = 32 / PAS_JS;                                     // stages per item
+  constexpr int SD = PAS_JS * NT;                                      // complex per half-stage
+  constexpr uint64_t ROWS = 1ull << H;
+  constexpr size_t PLANE = (size_t)1 << (N - 1);
+  constexpr int UNIT_D = PAS_NS * 2 * SD * 2 + padded(1 << L);        // doubles of smem per unit
+  extern __shared__ __align__(128) double smem[];
+  __shared__ __align__(8) uint64_t full[UNITS][PAS_NS];
+  __shared__ int used[UNITS][PAS_NS];
+  const int u = threadIdx.x / NT;
+  const uint32_t t = threadIdx.x % NT;
+  const int lane = threadIdx.x & 31;
+  double2* ring = reinterpret_cast<double2*>(smem + (size_t)u * UNIT_D);   // [NS][q | r][SD]
+  double* exch = smem + (size_t)u * UNIT_D + PAS_NS * 2 * SD * 2;
+  const BarNamed bar{1 + u, NT};
+  const uint64_t items = ROWS * (uint64_t)kcount;
+  const uint64_t first = (uint64_t)blockIdx.x * UNITS + u, step = (uint64_t)gridDim.x * UNITS;
+  const uint64_t my_items = items > first ? (items - 1 - first) / step + 1 : 0;
+  const uint64_t stages = my_items * SPI;
+  if (threadIdx.x == 0) {
+    for (int x = 0; x < UNITS; ++x)
+      for (int i = 0; i < PAS_NS; ++i) { mbar_init(&full[x][i], 1); used[x][i] = 0; }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  auto produce = [&](uint64_t st, int slot) {                   // one thread of the unit
+    const uint64_t item = first + (st / SPI) * step;
+    const uint32_t g = (uint32_t)(st % SPI);                    // j-blocks [JS g, JS g + JS)
+    const uint64_t yh = item / (uint64_t)kcount;
+    const uint64_t a = a_first + item % (uint64_t)kcount;
+    const int p = 63 - __clzll((long long)a);                   // >= L (a >= 2^L)
+    const uint64_t xh = ins0(yh, p - L);
+    const uint32_t ahi = (uint32_t)((a & ((1u << L) - 1u)) >> (L - 5));   // r block of block j is j ^ ahi
+    double2* dst = ring + (size_t)slot * 2 * SD;
+    mbar_expect_tx(&full[u][slot], 2 * SD * 16);
+    bulk_g2s(dst, psi + (xh << L) + (size_t)SD * g, SD * 16, &full[u][slot]);
+    // blocks {JS g + i} ^ ahi form the aligned group (g ^ (ahi / JS)) permuted by ahi % JS
+    bulk_g2s(dst + SD, psi + ((xh ^ (a >> L)) << L) + (size_t)SD * (g ^ (ahi / PAS_JS)), SD * 16, &full[u][slot]);
+  };
+  if (t == 0)
+    for (int i = 0; i < PAS_NS; ++i)
+      if ((uint64_t)i < stages) produce(i, i);
+  uint64_t st = 0;
+  for (uint64_t li = 0; li < my_items; ++li) {
+    const uint64_t item = first + li * step;
+    const uint64_t yh = item / (uint64_t)kcount;
+    const int k = (int)(item % (uint64_t)kcount);
+    const uint32_t al = (uint32_t)((a_first + (uint64_t)k) & ((1u << L) - 1u));
+    const uint32_t alo = al & (NT - 1), ahl = (al >> (L - 5)) % PAS_JS;
+    double v[2][32];
+#pragma unroll
+    for (int gi = 0; gi < SPI; ++gi, ++st) {
+      const int slot = (int)(st % PAS_NS);
+      mbar_wait(&full[u][slot], (uint32_t)(st / PAS_NS) & 1u);
+      const double2* c = ring + (size_t)slot * 2 * SD;
+#pragma unroll
+      for (int i = 0; i < PAS_JS; ++i) {
+        const int j = PAS_JS * gi + i;
+        const double2 q = c[NT * i + t];
+        const double2 r = c[SD + NT * (i ^ ahl) + (t ^ alo)];
+        v[0][j] = fma(r.x, q.x, r.y * q.y);
+        v[1][j] = fma(r.x, q.y, -(r.y * q.x));
+      }
+      __syncwarp();
+      int last = 0;
+      if (lane == 0) last = atomicAdd(&used[u][slot], 1) == WPU - 1;
+      if (__shfl_sync(0xffffffffu, last, 0) && lane == 0) {
+        atomicExch(&used[u][slot], 0);
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        if (st + PAS_NS < stages) produce(st + PAS_NS, slot);
+      }
+    }
+    Rounds<L, 0, 0, 2, BarNamed, true>::run(v, exch, t, bar);
+    // position pos = t + NT j (round-0 layout) -> slab-major ((pos >> CB) << (H+CB)) + (y_h << CB) + (pos & (C-1))
+    double* w0 = ws + (size_t)k * 2 * PLANE + (yh << CB);
+    constexpr uint32_t cm = (1u << CB) - 1u;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const uint32_t pos = t + NT * j;
+      const size_t off = ((size_t)(pos >> CB) << (H + CB)) + (pos & cm);
+      __stcg(w0 + off, v[0][j]);
+      __stcg(w0 + PLANE + off, v[1][j]);
+    }
+  }
 }
 
 // ------------------------------------------------------------------------------------------
@@ -858,6 +990,242 @@ __global__ void __launch_bounds__(256, 1) k_fused(const double2* __restrict__ ps
   }
 }
 
+// ==========================================================================================
+// TMEM path for N = 19, 20 (T = N-1 = L + 8).  Pass B gives every thread one workspace column of
+// 2^8 rows held in tensor memory, so the 8 row bits are transformed inside the thread with no
+// shared-memory exchange; pass A (L = 11 at N = 20) parks one plane in TMEM so a warp can own
+// 64 values per plane per lane (6 in-thread bits).  L1TEX data-pipe traffic per output value:
+// 16 B generation + 16 B exchange + 8 B store (A) + 8 B load (B) = 48 B.
+// Workspace: row-major planes [k][plane][y_h][pos], 2^L positions per row; pos low 5 bits are
+// y_l bits 5..9 (the lane index of pass A's final layout), so both passes access it coalesced.
+// ==========================================================================================
+// 32x32 transpose of one value per (lane, j) through a warp-private padded buffer:
+// element e = lane + 32 j is read back as e = j + 32 lane (conflict-free both ways)
+__device__ __forceinline__ void warp_transpose32(double (&v)[32], double* xw, int lane) {
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 32; ++j) xw[swz(lane + 32 * j)] = v[j];
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = xw[swz(j + 32 * lane)];
+}
+
+constexpr int PA11_NS = 2;                                                   // staging ring depth
+constexpr int PA11_SMEM = PA11_NS * 2 * 2048 * 16 + 8 * padded(1024) * 8;   // 128 KB ring + 66 KB exchange
+
+template <int N>
+__global__ void __launch_bounds__(256, 1) k_passA11t(const double2* __restrict__ psi, uint64_t a_first, int kcount,
+                                                     int groups, double* __restrict__ ws) {
+  constexpr int L = 11, H = N - 1 - L;
+  constexpr uint64_t ROWS = 1ull << H;
+  constexpr size_t PLANE = (size_t)1 << (N - 1);
+  extern __shared__ __align__(128) double smem[];
+  double2* ring = reinterpret_cast<double2*>(smem);             // [NS][q row | r row][2048]
+  double* exch = smem + PA11_NS * 2 * 2048 * 2;                 // [warp][padded 1024]
+  __shared__ __align__(8) uint64_t full[PA11_NS];
+  __shared__ int used[PA11_NS];
+  __shared__ uint32_t tbase;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t items = ROWS * (uint64_t)groups;
+  if (w == 0) tmem_alloc_warp(&tbase, 512);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < PA11_NS; ++i) { mbar_init(&full[i], 1); used[i] = 0; }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  // this warp's TMEM: lanes 32*(w%4).., columns (w/4)*256 ..; chunks A0 @0, B0 @64, B1 @128
+  const uint32_t tw = tbase + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)(w >> 2) * 256;
+  auto issue = [&](uint64_t item, int slot) {
+    const uint64_t g = item >> H, yh = item & (ROWS - 1);
+    const uint64_t ag = a_first + 8 * g;
+    const int p = 63 - __clzll((long long)ag);                  // >= 11 (a >= 2048)
+    const uint64_t xh = ins0(yh, p - L);
+    double2* dst = ring + (size_t)slot * 4096;
+    mbar_expect_tx(&full[slot], 2 * 2048 * 16);
+    bulk_g2s(dst, psi + (xh << L), 2048 * 16, &full[slot]);
+    bulk_g2s(dst + 2048, psi + ((xh ^ (ag >> L)) << L), 2048 * 16, &full[slot]);
+  };
+  if (threadIdx.x == 0)
+    for (int i = 0; i < PA11_NS; ++i)
+      if (blockIdx.x + (uint64_t)i * gridDim.x < items) issue(blockIdx.x + (uint64_t)i * gridDim.x, i);
+  double* xw = exch + (size_t)w * padded(1024);
+  uint32_t n = 0;
+  for (uint64_t item = blockIdx.x; item < items; item += gridDim.x, ++n) {
+    const int slot = (int)(n % PA11_NS);
+    mbar_wait(&full[slot], (n / PA11_NS) & 1u);
+    const uint64_t g = item >> H, yh = item & (ROWS - 1);
+    const int k = 8 * (int)g + w;
+    const bool active = k < kcount;
+    double lo[32], hi[32];
+    if (active) {
+      const uint32_t al = (uint32_t)((a_first + (uint64_t)k) & 2047u);
+      const double2* sq = ring + (size_t)slot * 4096;
+      // chunk c: y_l = lane + 32 j + 1024 c; registers j <-> y bits 5..9
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        double A[32], B[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const uint32_t yl = lane + 32 * j + 1024 * c;
+          const double2 q = sq[yl];
+          const double2 r = sq[2048 + (yl ^ al)];
+          A[j] = fma(r.x, q.x, r.y * q.y);
+          B[j] = fma(r.x, q.y, -(r.y * q.x));
+        }
+        bfly32<0, 5>(A);
+        bfly32<0, 5>(B);
+        if (c == 0) {
+          tmem_st32(tw + 0, A);
+          tmem_st32(tw + 64, B);
+        } else {
+          tmem_st32(tw + 128, B);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) hi[j] = A[j];
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0 && atomicAdd(&used[slot], 1) == 7) {          // ring slot read out by all 8 warps
+      atomicExch(&used[slot], 0);
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      const uint64_t nx = item + (uint64_t)PA11_NS * gridDim.x;
+      if (nx < items) issue(nx, slot);
+    }
+    if (active) {
+      tmem_wait_st();
+#pragma unroll
+      for (int pl = 0; pl < 2; ++pl) {
+        if (pl == 0) tmem_ld32(tw + 0, lo);                     // A0; A1 is already in hi
+        else { tmem_ld32(tw + 64, lo); tmem_ld32(tw + 128, hi); }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {                          // y bit 10
+          const double u = lo[j], v2 = hi[j];
+          lo[j] = u + v2;
+          hi[j] = u - v2;
+        }
+        // exchange each half: (lane <-> y bits 0-4, j <-> 5-9) -> (lane <-> 5-9, j <-> 0-4)
+        warp_transpose32(lo, xw, lane);
+        warp_transpose32(hi, xw, lane);
+        bfly32<0, 5>(lo);
+        bfly32<0, 5>(hi);
+        // position pos = lane + 32 j + 1024 h  (pos bits 0-4 = b_l bits 5-9, contiguous over lanes),
+        // stored chunk-major: ((pos >> 7) << 15) + row_off(y_h) + (pos & 127)
+        double* dst = ws + (size_t)k * 2 * PLANE + (size_t)pl * PLANE + cm_row_off(yh) + lane;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const size_t o = ((size_t)(j >> 2) << 15) + 32 * (j & 3);
+          __stcg(dst + o, lo[j]);
+          __stcg(dst + (8ull << 15) + o, hi[j]);
+        }
+      }
+    }
+  }
+  tmem_fence_before();
+  __syncthreads();
+  if (w == 0) tmem_dealloc_warp(tbase, 512);
+}
+
+// Pass B with the 8 row bits in TMEM: a CTA of 4 warps walks tiles (k, plane, 128-position
+// group); thread = one position (column), its 256 rows live in its TMEM lane (512 columns).
+// The tile streams in as 8 chunks (chunk c = rows {c + 8m}, m = 0..31) through a 4-deep ring of
+// 32 KB shared-memory buffers filled by bulk copies (one 1 KB row segment per lane), so global
+// latency is off the critical path.  Round 1: chunk c (row bits 3-7 in registers) is read from
+// shared memory, transformed and parked at TMEM columns 64c.  Round 2: groups of 4 m's across
+// the 8 chunks (row bits 0-2) come back from TMEM and feed the epilogue directly.
+constexpr int PB8_NS = 4;
+constexpr int PB8_SMEM = PB8_NS * 32 * 128 * 8;   // 4 x 32 KB
+
+template <int N, bool A2>
+__global__ void __launch_bounds__(128, 1) k_passBt8(int kcount, const double* __restrict__ ws, Alphas al,
+                                                    double* partial) {
+  constexpr int H = 8, L = N - 1 - H;
+  constexpr size_t PLANE = (size_t)1 << (N - 1);
+  constexpr uint64_t GROUPS = 1ull << (L - 7);                  // 128-position groups per plane
+  extern __shared__ __align__(128) double smem[];               // [NS][32 rows][128 positions]
+  __shared__ __align__(8) uint64_t full[PB8_NS];
+  __shared__ int used[PB8_NS];
+  __shared__ uint32_t tbase;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (w == 0) tmem_alloc_warp(&tbase, 512);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < PB8_NS; ++i) { mbar_init(&full[i], 1); used[i] = 0; }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tw = tbase + ((uint32_t)(32 * w) << 16);
+  const uint64_t tiles = (uint64_t)kcount * 2 * GROUPS;
+  const uint64_t my_tiles = tiles > blockIdx.x ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const uint64_t nchunks = my_tiles * 8;                        // chunk n: tile blockIdx + (n/8) grid, c = n%8
+  // a chunk (rows {c + 8m} of one 128-position group) is one contiguous 32 KB block (chunk-major)
+  auto issue = [&](uint64_t nch, int slot) {
+    if (lane != 0) return;
+    const uint64_t tile = blockIdx.x + (nch >> 3) * gridDim.x;
+    const int c = (int)(nch & 7);
+    const uint64_t kp = tile / GROUPS, grp = tile % GROUPS;
+    mbar_expect_tx(&full[slot], 32 * 128 * 8);
+    bulk_g2s(smem + (size_t)slot * 4096, ws + kp * PLANE + (grp << 15) + ((size_t)c << 12), 32 * 128 * 8, &full[slot]);
+  };
+  if (w == 0)
+    for (int i = 0; i < PB8_NS; ++i)
+      if ((uint64_t)i < nchunks) issue(i, i);
+  double acc[NACC];
+#pragma unroll
+  for (int i = 0; i < NACC; ++i) acc[i] = 0.0;
+  uint64_t n = 0;
+  for (uint64_t t = 0; t < my_tiles; ++t) {
+#pragma unroll 1
+    for (int c = 0; c < 8; ++c, ++n) {
+      const int slot = (int)(n % PB8_NS);
+      mbar_wait(&full[slot], (uint32_t)(n / PB8_NS) & 1u);
+      double v[32];
+      const double* buf = smem + (size_t)slot * 4096 + 32 * w + lane;
+#pragma unroll
+      for (int m = 0; m < 32; ++m) v[m] = buf[128 * m];
+      __syncwarp();
+      int last = 0;
+      if (lane == 0) last = atomicAdd(&used[slot], 1) == 3;     // last of the 4 warps to read it
+      if (__shfl_sync(0xffffffffu, last, 0)) {
+        if (lane == 0) atomicExch(&used[slot], 0);
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        if (n + PB8_NS < nchunks) issue(n + PB8_NS, slot);
+      }
+      bfly32<0, 5>(v);
+      tmem_st32(tw + 64 * c, v);
+    }
+    tmem_wait_st();
+    double loc[NACC];
+#pragma unroll
+    for (int i = 0; i < NACC; ++i) loc[i] = 0.0;
+#pragma unroll 1
+    for (int q = 0; q < 8; ++q) {
+      double u[32];                                             // u[4c + i] = row c + 8 (4q + i)
+      tmem_ld4x8(tw + 8 * q, u);
+#pragma unroll
+      for (int b = 2; b < 5; ++b) {                             // register bits 2-4 <-> row bits 0-2
+        const int hh = 1 << b;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          if (i & hh) continue;
+          const double x = u[i], y = u[i + hh];
+          u[i] = x + y;
+          u[i + hh] = x - y;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j) Epi<A2>::add(loc, u[j], al);
+    }
+#pragma unroll
+    for (int i = 0; i < NACC; ++i) acc[i] += loc[i];
+  }
+  tmem_fence_before();
+  block_flush(acc, partial, blockIdx.x);
+  if (w == 0) tmem_dealloc_warp(tbase, 512);
+}
+
 // ------------------------------------------------------------------------------------------
 // reduction of per-CTA partials (fixed order) + rescale t = 4 t' (DESIGN "Half-length").
 //   out[s*(n+2)+i] = scale_i * sum_slot partial[s][slot][i]
@@ -871,18 +1239,31 @@ struct ReduceArgs {
   double scale4[MAXA];  // 4^alpha_i
   const int* err;   // nonzero => a persistent kernel's watchdog fired: results are NaN
 };
-__global__ void k_reduce(const double* __restrict__ partial, ReduceArgs r, double* out) {
-  // one block (one warp) per state; column sums over slots in fixed order
+__global__ void __launch_bounds__(256) k_reduce(const double* __restrict__ partial, ReduceArgs r, double* out) {
+  // one block per state; thread i sums slots i, i+256, ... in order, then a fixed binary tree
+  // over the 256 thread sums: deterministic for a given nslots
   const int s = blockIdx.x;
   const double* base = partial + (size_t)s * r.nslots * NACC;
+  __shared__ double red[NACC][256];
   __shared__ double col[NACC];
   const int i = threadIdx.x;
-  if (i < NACC) {
-    double acc = 0.0;
-    for (int k = 0; k < r.nslots; ++k) acc += base[(size_t)k * NACC + i];
-    col[i] = acc;
+  double acc[NACC];
+#pragma unroll
+  for (int c = 0; c < NACC; ++c) acc[c] = 0.0;
+  for (int k = i; k < r.nslots; k += 256)
+#pragma unroll
+    for (int c = 0; c < NACC; ++c) acc[c] += base[(size_t)k * NACC + c];
+#pragma unroll
+  for (int c = 0; c < NACC; ++c) red[c][i] = acc[c];
+  __syncthreads();
+  for (int h = 128; h > 0; h >>= 1) {
+    if (i < h)
+#pragma unroll
+      for (int c = 0; c < NACC; ++c) red[c][i] += red[c][i + h];
+    __syncthreads();
   }
-  __syncwarp();
+  if (i < NACC) col[i] = red[i][0];
+  __syncthreads();
   if (i == 0) {
     double* o = out + (size_t)s * (r.n_alpha + 2);
     if (r.err && *r.err) {
