@@ -47,6 +47,14 @@ typedef enum {
 #define SRE_MAX_N 26
 #define SRE_MAX_ALPHA 16
 
+/* Arithmetic of the transform (north star: FP64, with an optional FP32 mode).
+ *   SRE_FP64: generation, Walsh-Hadamard transform, workspace and power sums in FP64
+ *             (tolerance vs the oracle: S_alpha relative 1e-10).
+ *   SRE_FP32: psi converted to complex64 once; generation, transform and workspace in FP32;
+ *             each thread's 32-value tile summed in FP32, accumulated in FP64
+ *             (tolerance: S_alpha relative 1e-4; halves the bytes moved per Pauli string). */
+typedef enum { SRE_FP64 = 0, SRE_FP32 = 1 } sre_precision;
+
 /* Static string for a status code. */
 const char* sre_status_string(int code);
 /* Thread-local detail of the last error (empty string if none). */
@@ -97,6 +105,18 @@ size_t sre_workspace_size(int N, int B, int n_alpha);
 int sre_partial_sums(const void* psi, int N, int B, uint64_t a_begin, uint64_t a_end,
                      const double* alpha, int n_alpha, void* workspace, size_t ws_bytes,
                      double* sums_dev, void* stream);
+
+/*
+ * Precision-selecting variants (precision = sre_precision); the plain entry points are SRE_FP64.
+ * sre_exact_ex takes B states like sre_exact_batched.  Unknown precision -> SRE_EINVAL (0 bytes
+ * from sre_workspace_size_ex).
+ */
+size_t sre_workspace_size_ex(int N, int B, int n_alpha, int precision);
+int sre_exact_ex(const void* psi, int N, int B, const double* alpha, int n_alpha, int precision, double* out_M,
+                 double* out_lost_norm);
+int sre_partial_sums_ex(const void* psi, int N, int B, uint64_t a_begin, uint64_t a_end, const double* alpha,
+                        int n_alpha, int precision, void* workspace, size_t ws_bytes, double* sums_dev,
+                        void* stream);
 
 /*
  * sre_finalize -- host-side Eq. (2) from complete sums (all 2^N X-strings):

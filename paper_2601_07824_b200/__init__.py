@@ -23,6 +23,8 @@ LIB_PATH = os.path.join(_HERE, "libsre_b200.so")
 __all__ = ["SreError", "load", "exact", "exact_batched", "partial_sums", "finalize", "workspace_size",
            "chi", "norm2", "launch_count", "profile_begin", "profile_end", "LIB_PATH"]
 
+PRECISION = {"fp64": 0, "fp32": 1}   # sre_precision (include/sre.h)
+
 _STATUS = {0: "SRE_OK", 1: "SRE_EINVAL", 2: "SRE_ERANGE", 3: "SRE_ENOTNORM", 4: "SRE_EWORKSPACE",
            5: "SRE_ENOMEM", 6: "SRE_ECUDA", 7: "SRE_EINTERNAL", 8: "SRE_ENODEV"}
 
@@ -56,6 +58,9 @@ def load():
             "sre_finalize": ([dp, i, i, dp, i, dp, dp], i),
             "sre_norm2": ([vp, i, i, vp, vp], i),
             "sre_chi": ([vp, i, u64, vp, vp], i),
+            "sre_workspace_size_ex": ([i, i, i, i], ctypes.c_size_t),
+            "sre_exact_ex": ([vp, i, i, dp, i, i, dp, dp], i),
+            "sre_partial_sums_ex": ([vp, i, i, u64, u64, dp, i, i, vp, ctypes.c_size_t, vp, vp], i),
             "sre_launch_count": ([], u64),
             "sre_profile_begin": ([i], i),
             "sre_profile_end": ([dp, ctypes.POINTER(u64), ctypes.POINTER(u64)], i),
@@ -110,9 +115,16 @@ def _psi_ptr(psi):
     return a.ctypes.data, _nqubits(a.shape[-1]), b, a
 
 
-def exact(psi, alphas: Sequence[float] = (2.0,)):
+def _prec(precision: str) -> int:
+    if precision not in PRECISION:
+        raise SreError(1, f"precision {precision!r}: one of {sorted(PRECISION)}")
+    return PRECISION[precision]
+
+
+def exact(psi, alphas: Sequence[float] = (2.0,), precision: str = "fp64"):
     """M_alpha (bits) and lost_norm of one state -- Eq. (2) via Alg. 2 over all 2^N X-strings.
-    psi: complex128 torch tensor (cuda: no copy; cpu) or numpy array (host: copied by the call)."""
+    psi: complex128 torch tensor (cuda: no copy; cpu) or numpy array (host: copied by the call).
+    precision "fp32" selects the optional FP32 transform (FP64 accumulation, ~1e-4 relative)."""
     lib = load()
     ptr, n, b, keep = _psi_ptr(psi)
     if b != 1:
@@ -120,28 +132,33 @@ def exact(psi, alphas: Sequence[float] = (2.0,)):
     al = _alphas(alphas)
     out = np.zeros(al.size)
     ln = ctypes.c_double(0.0)
-    _check(lib.sre_exact(ctypes.c_void_p(ptr), n, _dp(al), al.size, _dp(out), ctypes.pointer(ln)))
+    if precision == "fp64":
+        _check(lib.sre_exact(ctypes.c_void_p(ptr), n, _dp(al), al.size, _dp(out), ctypes.pointer(ln)))
+    else:
+        _check(lib.sre_exact_ex(ctypes.c_void_p(ptr), n, 1, _dp(al), al.size, _prec(precision), _dp(out),
+                                ctypes.pointer(ln)))
     del keep
     return [float(x) for x in out], ln.value
 
 
-def exact_batched(psi, alphas: Sequence[float] = (2.0,)):
+def exact_batched(psi, alphas: Sequence[float] = (2.0,), precision: str = "fp64"):
     """[B][n_alpha] M values and [B] lost_norms for a batch psi[B, 2^N]."""
     lib = load()
     ptr, n, b, keep = _psi_ptr(psi)
     al = _alphas(alphas)
     out = np.zeros((b, al.size))
     ln = np.zeros(b)
-    _check(lib.sre_exact_batched(ctypes.c_void_p(ptr), n, b, _dp(al), al.size, _dp(out), _dp(ln)))
+    _check(lib.sre_exact_ex(ctypes.c_void_p(ptr), n, b, _dp(al), al.size, _prec(precision), _dp(out), _dp(ln)))
     del keep
     return out, ln
 
 
-def workspace_size(n: int, b: int = 1, n_alpha: int = 1) -> int:
-    return int(load().sre_workspace_size(n, b, n_alpha))
+def workspace_size(n: int, b: int = 1, n_alpha: int = 1, precision: str = "fp64") -> int:
+    return int(load().sre_workspace_size_ex(n, b, n_alpha, _prec(precision)))
 
 
-def partial_sums(psi, a_begin: int, a_end: int, alphas: Sequence[float], out=None, workspace=None, stream=None):
+def partial_sums(psi, a_begin: int, a_end: int, alphas: Sequence[float], out=None, workspace=None, stream=None,
+                 precision: str = "fp64"):
     """Raw sums [B, n_alpha+2] (S_alpha..., S_1, sum t ln t) over X-strings a in [a_begin, a_end),
     enqueued on ``stream`` (default: torch's current stream).  psi must be a cuda tensor."""
     import torch
@@ -153,13 +170,13 @@ def partial_sums(psi, a_begin: int, a_end: int, alphas: Sequence[float], out=Non
     dev = psi.device
     if out is None:
         out = torch.empty((b, al.size + 2), dtype=torch.float64, device=dev)
-    ws_need = workspace_size(n, b, al.size)
+    ws_need = workspace_size(n, b, al.size, precision)
     if workspace is None or workspace.numel() < ws_need:
         workspace = torch.empty(ws_need, dtype=torch.uint8, device=dev)
     st = stream if stream is not None else torch.cuda.current_stream(dev)
-    _check(lib.sre_partial_sums(ctypes.c_void_p(ptr), n, b, int(a_begin), int(a_end), _dp(al), al.size,
-                                ctypes.c_void_p(workspace.data_ptr()), workspace.numel(),
-                                ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(st.cuda_stream)))
+    _check(lib.sre_partial_sums_ex(ctypes.c_void_p(ptr), n, b, int(a_begin), int(a_end), _dp(al), al.size,
+                                   _prec(precision), ctypes.c_void_p(workspace.data_ptr()), workspace.numel(),
+                                   ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(st.cuda_stream)))
     del keep
     return out
 

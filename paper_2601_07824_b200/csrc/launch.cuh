@@ -1,0 +1,336 @@
+// launch.cuh -- host-side launch templates shared by the kernel-family translation units.
+// Each family .cu file (k_small.cu, k_mid.cu, k_generic.cu, k_stageA.cu, k_stageB.cu, k_exp.cu)
+// explicitly instantiates its dispatchers; sre_api.cu sees them as extern templates, so the
+// kernels compile once each and in parallel (paper_2601_07824_b200/_build.py).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <cstdlib>
+#include <mutex>
+#include <type_traits>
+#include <utility>
+#include <vector>
+
+#include "../../include/sre.h"
+#include "sre_kernels.cuh"
+
+namespace sre_host {
+using namespace sre;
+
+enum LaunchKind { LK_SINGLE = 0, LK_PASSA = 1, LK_PASSB = 2, LK_AUX = 3, LK_FUSED = 4, LK_N = 5 };
+
+struct Prof {
+  std::mutex mu;
+  bool on = false;
+  int stride = 1;
+  uint64_t launched[LK_N] = {0, 0, 0, 0, 0};
+  std::vector<cudaEvent_t> pool;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed[LK_N];
+};
+extern Prof g_prof;
+extern std::atomic<uint64_t> g_launches;
+cudaEvent_t prof_event();
+
+// Wraps one kernel launch: counts it, and when profiling, brackets every stride-th launch of
+// its kind with CUDA events on the launching stream.
+template <class F>
+cudaError_t launch_counted(int kind, cudaStream_t st, F&& f) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (!g_prof.on) return f();
+  std::lock_guard<std::mutex> lk(g_prof.mu);
+  const bool sample = (g_prof.launched[kind]++ % (uint64_t)g_prof.stride) == 0;
+  if (!sample) return f();
+  cudaEvent_t a = prof_event(), b = prof_event();
+  cudaEventRecord(a, st);
+  cudaError_t e = f();
+  cudaEventRecord(b, st);
+  g_prof.timed[kind].push_back({a, b});
+  return e;
+}
+
+struct Dev {
+  int id = -1, sms = 0, major = 0, minor = 0;
+};
+
+enum Kind { SMALL = 0, MID = 1, TWOPASS = 2 };
+
+struct Plan {
+  int N = 0, T = 0, kind = 0;
+  int L = 0, H = 0, CB = 0, TP = 0, K = 0;  // two-pass
+  int unitsA = 0, unitsB = 0, blkB = 0;
+  size_t slab_doubles = 0;  // K * 2^N
+  size_t slots = 0;         // partial slots per state
+  bool staged = false;      // L == 10: k_passA10s + k_passBp
+  bool tmem = false;        // N = 19, 20: TMEM pass B (H = 8) + k_passA11t / k_passA10s<RM>
+  uint64_t amin = 0;        // first X-string the staged / TMEM kernels accept (a_h != 0)
+  int KG = 0;               // 8-X-string groups per staged launch
+};
+
+bool tmem_enabled();
+
+// ------------------------------------------------------------------------------------------
+// launchers (template dispatch)
+// ------------------------------------------------------------------------------------------
+template <class V, int T, bool A2, bool DBG>
+cudaError_t launch_small_t(const typename Cx<V>::T* psi, int N, int B, int gx, uint64_t a0, uint64_t count, const Alphas& al,
+                           double* partial, double* chi, cudaStream_t st) {
+  dim3 grid(gx, B);
+  return launch_counted(LK_SINGLE, st, [&] {
+    k_small<T, A2, DBG, V><<<grid, 256, 0, st>>>(psi, N, a0, count, al, partial, chi);
+    return cudaGetLastError();
+  });
+}
+
+template <class V, bool A2, bool DBG>
+cudaError_t launch_small(int T, const typename Cx<V>::T* psi, int N, int B, int gx, uint64_t a0, uint64_t count, const Alphas& al,
+                         double* partial, double* chi, cudaStream_t st) {
+  switch (T) {
+#define C_(t) case t: return launch_small_t<V, t, A2, DBG>(psi, N, B, gx, a0, count, al, partial, chi, st);
+    C_(0) C_(1) C_(2) C_(3) C_(4) C_(5) C_(6) C_(7) C_(8) C_(9) C_(10)
+#undef C_
+  }
+  return cudaErrorInvalidValue;
+}
+
+constexpr int SMEM_128K = 2 * padded(32 * 256) * 8;  // 2 planes x (2^T + pad) x UPC units
+
+template <class K>
+cudaError_t set_smem(K kern, int bytes) {
+  return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+template <class V, int T, bool A2, bool DBG>
+cudaError_t launch_mid_t(const typename Cx<V>::T* psi, int N, int B, int gx, uint64_t a0, uint64_t count, const Alphas& al,
+                         double* partial, double* chi, cudaStream_t st) {
+  static bool init = false;
+  if (!init) {
+    cudaError_t e = set_smem(k_mid<T, A2, DBG, V>, SMEM_128K);
+    if (e != cudaSuccess) return e;
+    init = true;
+  }
+  dim3 grid(gx, B);
+  return launch_counted(LK_SINGLE, st, [&] {
+    k_mid<T, A2, DBG, V><<<grid, 256, SMEM_128K, st>>>(psi, N, a0, count, al, partial, chi);
+    return cudaGetLastError();
+  });
+}
+
+template <class V, bool A2, bool DBG>
+cudaError_t launch_mid(int T, const typename Cx<V>::T* psi, int N, int B, int gx, uint64_t a0, uint64_t count, const Alphas& al,
+                       double* partial, double* chi, cudaStream_t st) {
+  switch (T) {
+    case 11: return launch_mid_t<V, 11, A2, DBG>(psi, N, B, gx, a0, count, al, partial, chi, st);
+    case 12: return launch_mid_t<V, 12, A2, DBG>(psi, N, B, gx, a0, count, al, partial, chi, st);
+    case 13: return launch_mid_t<V, 13, A2, DBG>(psi, N, B, gx, a0, count, al, partial, chi, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <class V, int L>
+cudaError_t launch_passA_t(const typename Cx<V>::T* psi, int N, uint64_t a0, int kcount, V* ws, int units, cudaStream_t st) {
+  static bool init = false;
+  if (!init) {
+    cudaError_t e = set_smem(k_passA<L, V>, SMEM_128K);
+    if (e != cudaSuccess) return e;
+    init = true;
+  }
+  const uint64_t items = (uint64_t)kcount << (N - 1 - L);
+  const unsigned grid = (unsigned)((items + units - 1) / units);
+  return launch_counted(LK_PASSA, st, [&] {
+    k_passA<L, V><<<grid, 256, SMEM_128K, st>>>(psi, N, a0, kcount, ws);
+    return cudaGetLastError();
+  });
+}
+
+template <class V>
+cudaError_t launch_passA(const Plan& p, const typename Cx<V>::T* psi, uint64_t a0, int kcount, V* ws, cudaStream_t st) {
+  switch (p.L) {
+    case 10: return launch_passA_t<V, 10>(psi, p.N, a0, kcount, ws, p.unitsA, st);
+    case 11: return launch_passA_t<V, 11>(psi, p.N, a0, kcount, ws, p.unitsA, st);
+    case 12: return launch_passA_t<V, 12>(psi, p.N, a0, kcount, ws, p.unitsA, st);
+    case 13: return launch_passA_t<V, 13>(psi, p.N, a0, kcount, ws, p.unitsA, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <class V, int TP, int CB, bool A2, bool DBG>
+cudaError_t launch_passB_t(const Plan& p, uint64_t a0, int kcount, const V* ws, const Alphas& al, double* partial,
+                           double* chi, cudaStream_t st) {
+  constexpr int BLK = TP >= 14 ? 512 : 256;
+  constexpr int SM = padded(BLK * 32) * 8;
+  static bool init = false;
+  if (!init) {
+    cudaError_t e = set_smem(k_passB<TP, CB, A2, DBG, V>, SM);
+    if (e != cudaSuccess) return e;
+    init = true;
+  }
+  const uint64_t items = (uint64_t)kcount * 2 * (1ull << (p.L - CB));
+  const unsigned grid = (unsigned)((items + p.unitsB - 1) / p.unitsB);
+  return launch_counted(LK_PASSB, st, [&] {
+    k_passB<TP, CB, A2, DBG, V><<<grid, BLK, SM, st>>>(p.N, p.L, a0, kcount, ws, al, partial, chi);
+    return cudaGetLastError();
+  });
+}
+
+template <class V, bool A2, bool DBG>
+cudaError_t launch_passB(const Plan& p, uint64_t a0, int kcount, const V* ws, const Alphas& al, double* partial,
+                         double* chi, cudaStream_t st) {
+  const int key = p.TP * 16 + p.CB;
+  switch (key) {
+#define C_(tp, cb) case tp * 16 + cb: return launch_passB_t<V, tp, cb, A2, DBG>(p, a0, kcount, ws, al, partial, chi, st);
+    C_(10, 6) C_(11, 6) C_(12, 6) C_(13, 6) C_(13, 5) C_(13, 4) C_(13, 3) C_(13, 2) C_(14, 2)
+#undef C_
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <class V, int N>
+cudaError_t launch_passA10s_t(const Dev& d, const typename Cx<V>::T* psi, uint64_t a_first, int kcount, V* ws,
+                              cudaStream_t st) {
+  static bool init = false;
+  if (!init) {
+    cudaError_t e = set_smem(k_passA10s<N, false, V>, PA10_SMEM);
+    if (e != cudaSuccess) return e;
+    init = true;
+  }
+  const int groups = (kcount + 7) / 8;
+  const uint64_t items = (uint64_t)groups << (N - 11);
+  const unsigned grid = (unsigned)(items < (uint64_t)d.sms ? items : (uint64_t)d.sms);
+  return launch_counted(LK_PASSA, st, [&] {
+    k_passA10s<N, false, V><<<grid, 256, PA10_SMEM, st>>>(psi, a_first, kcount, groups, ws);
+    return cudaGetLastError();
+  });
+}
+
+cudaError_t launch_tmem_pair(const Plan& p, const Dev& d, bool a2, const double2* psi, uint64_t a_first, int kcount,
+                             double* ws, const Alphas& al, double* partial, cudaStream_t st);
+
+template <class V, int N, int L>
+cudaError_t launch_passAs_t(const Dev& d, const typename Cx<V>::T* psi, uint64_t a_first, int kcount, V* ws,
+                            cudaStream_t st) {
+  static bool init = false;
+  if (!init) {
+    cudaError_t e = set_smem(k_passAs<N, L, V>, pas_smem(L));
+    if (e != cudaSuccess) return e;
+    init = true;
+  }
+  const uint64_t units = (uint64_t)kcount << (N - 1 - L);
+  const uint64_t ctas = (units + (256 >> (L - 5)) - 1) / (256 >> (L - 5));
+  const unsigned grid = (unsigned)(ctas < (uint64_t)d.sms ? ctas : (uint64_t)d.sms);
+  return launch_counted(LK_PASSA, st, [&] {
+    k_passAs<N, L, V><<<grid, 256, pas_smem(L), st>>>(psi, a_first, kcount, ws);
+    return cudaGetLastError();
+  });
+}
+
+template <class V>
+cudaError_t launch_passA10s(const Plan& p, const Dev& d, const typename Cx<V>::T* psi, uint64_t a_first, int kcount,
+                            V* ws, cudaStream_t st) {
+  switch (p.N) {
+    case 21: return launch_passAs_t<V, 21, 12>(d, psi, a_first, kcount, ws, st);
+    case 22: return launch_passAs_t<V, 22, 12>(d, psi, a_first, kcount, ws, st);
+    case 23: return launch_passAs_t<V, 23, 12>(d, psi, a_first, kcount, ws, st);
+    case 24: return launch_passAs_t<V, 24, 12>(d, psi, a_first, kcount, ws, st);
+    case 25: return launch_passAs_t<V, 25, 13>(d, psi, a_first, kcount, ws, st);
+    case 15: return launch_passA10s_t<V, 15>(d, psi, a_first, kcount, ws, st);
+    case 16: return launch_passA10s_t<V, 16>(d, psi, a_first, kcount, ws, st);
+    case 17: return launch_passA10s_t<V, 17>(d, psi, a_first, kcount, ws, st);
+    case 18: return launch_passA10s_t<V, 18>(d, psi, a_first, kcount, ws, st);
+    case 19: return launch_passA10s_t<V, 19>(d, psi, a_first, kcount, ws, st);
+    case 20: return launch_passA10s_t<V, 20>(d, psi, a_first, kcount, ws, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+bool fused_enabled();
+template <bool A2>
+cudaError_t launch_fused(const Plan& p, const Dev& d, const double2* psi, uint64_t a_first, uint64_t count,
+                         double* ws, FusedCtl* ctl, const Alphas& al, double* partial, cudaStream_t st);
+
+template <class V, int TP, int CB, bool A2>
+cudaError_t launch_passBt_t(const Plan& p, const Dev& d, int kcount, const V* ws, const Alphas& al,
+                            double* partial, cudaStream_t st) {
+  static bool init = false;
+  if (!init) {
+    cudaError_t e = set_smem(k_passBt<TP, CB, A2, V>, pbt_smem(TP));
+    if (e != cudaSuccess) return e;
+    init = true;
+  }
+  const unsigned grid = (unsigned)d.sms;
+  return launch_counted(LK_PASSB, st, [&] {
+    k_passBt<TP, CB, A2, V><<<grid, 256, pbt_smem(TP), st>>>(p.N, kcount, ws, al, partial);
+    return cudaGetLastError();
+  });
+}
+
+template <class V, bool A2>
+cudaError_t launch_passBp(const Plan& p, const Dev& d, int kcount, const V* ws, const Alphas& al, double* partial,
+                          cudaStream_t st) {
+  if (p.N >= 21) {     // streamed path: tiles of 2^13 doubles, CB = 13 - H
+    switch (13 - p.H) {
+      case 7: return launch_passBt_t<V, 13, 7, A2>(p, d, kcount, ws, al, partial, st);
+      case 6: return launch_passBt_t<V, 13, 6, A2>(p, d, kcount, ws, al, partial, st);
+      case 5: return launch_passBt_t<V, 13, 5, A2>(p, d, kcount, ws, al, partial, st);
+      case 4: return launch_passBt_t<V, 13, 4, A2>(p, d, kcount, ws, al, partial, st);
+      case 3: return launch_passBt_t<V, 13, 3, A2>(p, d, kcount, ws, al, partial, st);
+      case 2: return launch_passBt_t<V, 13, 2, A2>(p, d, kcount, ws, al, partial, st);
+    }
+    return cudaErrorInvalidValue;
+  }
+  switch (12 - p.H) {  // slab-major tiles of 2^12 doubles: CB = 12 - H
+    case 8: return launch_passBt_t<V, 12, 8, A2>(p, d, kcount, ws, al, partial, st);
+    case 7: return launch_passBt_t<V, 12, 7, A2>(p, d, kcount, ws, al, partial, st);
+    case 6: return launch_passBt_t<V, 12, 6, A2>(p, d, kcount, ws, al, partial, st);
+    case 5: return launch_passBt_t<V, 12, 5, A2>(p, d, kcount, ws, al, partial, st);
+    case 4: return launch_passBt_t<V, 12, 4, A2>(p, d, kcount, ws, al, partial, st);
+    case 3: return launch_passBt_t<V, 12, 3, A2>(p, d, kcount, ws, al, partial, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+
+// ------------------------------------------------------------------------------------------
+// explicit instantiations: defined in the family translation units
+// ------------------------------------------------------------------------------------------
+#define SRE_SIG_SMALL(V, A2, DBG) cudaError_t launch_small<V, A2, DBG>(int, const typename Cx<V>::T*, int, int, int, \
+    uint64_t, uint64_t, const Alphas&, double*, double*, cudaStream_t)
+#define SRE_SIG_MID(V, A2, DBG) cudaError_t launch_mid<V, A2, DBG>(int, const typename Cx<V>::T*, int, int, int, \
+    uint64_t, uint64_t, const Alphas&, double*, double*, cudaStream_t)
+#define SRE_SIG_PASSA(V) cudaError_t launch_passA<V>(const Plan&, const typename Cx<V>::T*, uint64_t, int, V*, cudaStream_t)
+#define SRE_SIG_PASSB(V, A2, DBG) cudaError_t launch_passB<V, A2, DBG>(const Plan&, uint64_t, int, const V*, \
+    const Alphas&, double*, double*, cudaStream_t)
+#define SRE_SIG_STAGEA(V) cudaError_t launch_passA10s<V>(const Plan&, const Dev&, const typename Cx<V>::T*, uint64_t, \
+    int, V*, cudaStream_t)
+#define SRE_SIG_STAGEB(V, A2) cudaError_t launch_passBp<V, A2>(const Plan&, const Dev&, int, const V*, const Alphas&, \
+    double*, cudaStream_t)
+#define SRE_SIG_FUSED(A2) cudaError_t launch_fused<A2>(const Plan&, const Dev&, const double2*, uint64_t, uint64_t, \
+    double*, FusedCtl*, const Alphas&, double*, cudaStream_t)
+#define SRE_FOR_V_A2_DBG(M, P) P M(double, true, false); P M(double, false, false); P M(float, true, false); \
+    P M(float, false, false); P M(double, false, true)
+#define SRE_FOR_V(M, P) P M(double); P M(float)
+#define SRE_FOR_V_A2(M, P) P M(double, true); P M(double, false); P M(float, true); P M(float, false)
+
+#ifndef SRE_FAMILY_SMALL
+SRE_FOR_V_A2_DBG(SRE_SIG_SMALL, extern template);
+#endif
+#ifndef SRE_FAMILY_MID
+SRE_FOR_V_A2_DBG(SRE_SIG_MID, extern template);
+#endif
+#ifndef SRE_FAMILY_GENERIC
+SRE_FOR_V(SRE_SIG_PASSA, extern template);
+SRE_FOR_V_A2_DBG(SRE_SIG_PASSB, extern template);
+#endif
+#ifndef SRE_FAMILY_STAGEA
+SRE_FOR_V(SRE_SIG_STAGEA, extern template);
+#endif
+#ifndef SRE_FAMILY_STAGEB
+SRE_FOR_V_A2(SRE_SIG_STAGEB, extern template);
+#endif
+#ifndef SRE_FAMILY_EXP
+extern template SRE_SIG_FUSED(true);
+extern template SRE_SIG_FUSED(false);
+#endif
+
+}  // namespace sre_host

@@ -9,14 +9,17 @@
 #include <cstring>
 #include <atomic>
 #include <mutex>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/sre.h"
-#include "sre_kernels.cuh"
+#define SRE_API_TU
+#include "launch.cuh"
 
 using namespace sre;
+using namespace sre_host;
 
-namespace {
+namespace sre_host {
 
 thread_local char g_err[512] = "";
 
@@ -38,16 +41,6 @@ int fail(int code, const char* fmt, ...) {
 // ------------------------------------------------------------------------------------------
 // launch accounting and sampled per-kernel timing (bench.py's roofline numbers)
 // ------------------------------------------------------------------------------------------
-enum LaunchKind { LK_SINGLE = 0, LK_PASSA = 1, LK_PASSB = 2, LK_AUX = 3, LK_FUSED = 4, LK_N = 5 };
-
-struct Prof {
-  std::mutex mu;
-  bool on = false;
-  int stride = 1;
-  uint64_t launched[LK_N] = {0, 0, 0, 0, 0};
-  std::vector<cudaEvent_t> pool;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed[LK_N];
-};
 Prof g_prof;
 std::atomic<uint64_t> g_launches{0};
 
@@ -62,26 +55,6 @@ cudaEvent_t prof_event() {
   return e;
 }
 
-// Wraps one kernel launch: counts it, and when profiling, brackets every stride-th launch of
-// its kind with CUDA events on the launching stream.
-template <class F>
-cudaError_t launch_counted(int kind, cudaStream_t st, F&& f) {
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  if (!g_prof.on) return f();
-  std::lock_guard<std::mutex> lk(g_prof.mu);
-  const bool sample = (g_prof.launched[kind]++ % (uint64_t)g_prof.stride) == 0;
-  if (!sample) return f();
-  cudaEvent_t a = prof_event(), b = prof_event();
-  cudaEventRecord(a, st);
-  cudaError_t e = f();
-  cudaEventRecord(b, st);
-  g_prof.timed[kind].push_back({a, b});
-  return e;
-}
-
-struct Dev {
-  int id = -1, sms = 0, major = 0, minor = 0;
-};
 
 int get_dev(Dev& d) {
   int id = 0;
@@ -107,20 +80,6 @@ int get_dev(Dev& d) {
 // ------------------------------------------------------------------------------------------
 // plan
 // ------------------------------------------------------------------------------------------
-enum Kind { SMALL = 0, MID = 1, TWOPASS = 2 };
-
-struct Plan {
-  int N = 0, T = 0, kind = 0;
-  int L = 0, H = 0, CB = 0, TP = 0, K = 0;  // two-pass
-  int unitsA = 0, unitsB = 0, blkB = 0;
-  size_t slab_doubles = 0;  // K * 2^N
-  size_t slots = 0;         // partial slots per state
-  bool staged = false;      // L == 10: k_passA10s + k_passBp
-  bool tmem = false;        // N = 19, 20: TMEM pass B (H = 8) + k_passA11t / k_passA10s<RM>
-  uint64_t amin = 0;        // first X-string the staged / TMEM kernels accept (a_h != 0)
-  int KG = 0;               // 8-X-string groups per staged launch
-};
-
 bool tmem_enabled() {  // opt-in (SRE_TMEM=1): the 4-warp TMEM pass B measured slower (37 vs 30 us)
   const char* e = getenv("SRE_TMEM");
   return e && e[0] == '1';
@@ -211,17 +170,18 @@ int make_plan(int N, const Dev& d, Plan& p) {
   return SRE_OK;
 }
 
-size_t ws_bytes_for(const Plan& p, int B) {
-  size_t partial = p.slots * NACC * (p.kind == TWOPASS ? 1 : (size_t)B);
-  size_t norm = 4096 * (size_t)B + (size_t)B;
-  return (partial + p.slab_doubles + norm + 64) * sizeof(double) + 256;   // + FusedCtl
+// Workspace layout (bytes, every region 256-B aligned for bulk copies):
+//   [partial slots][slab][norm scratch][FusedCtl][psi as complex64 (FP32 mode only)]
+constexpr size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+size_t off_slab(const Plan& p, int B) { return align256(p.slots * NACC * (p.kind == TWOPASS ? 1 : (size_t)B) * 8); }
+size_t off_norm(const Plan& p, int B) { return off_slab(p, B) + align256(p.slab_doubles * 8); }
+size_t off_ctl(const Plan& p, int B) { return off_norm(p, B) + align256((4096 * (size_t)B + (size_t)B) * 8); }
+size_t off_psi32(const Plan& p, int B) { return off_ctl(p, B) + align256(sizeof(FusedCtl)); }
+size_t ws_bytes_for(const Plan& p, int B, int prec = 0) {
+  return off_psi32(p, B) + (prec ? align256(((size_t)B << p.N) * sizeof(float2)) : 0);
 }
-// FusedCtl lives after the norm area
-FusedCtl* ctl_of(char* ws, const Plan& p, int B) {
-  size_t partial = p.slots * NACC * (p.kind == TWOPASS ? 1 : (size_t)B);
-  size_t norm = 4096 * (size_t)B + (size_t)B;
-  return reinterpret_cast<FusedCtl*>(reinterpret_cast<double*>(ws) + partial + p.slab_doubles + norm);
-}
+FusedCtl* ctl_of(char* ws, const Plan& p, int B) { return reinterpret_cast<FusedCtl*>(ws + off_ctl(p, B)); }
+float2* psi32_of(char* ws, const Plan& p, int B) { return reinterpret_cast<float2*>(ws + off_psi32(p, B)); }
 
 // ------------------------------------------------------------------------------------------
 // alpha sweeps
@@ -261,298 +221,9 @@ std::vector<Sweep> make_sweeps(const double* alpha, int n_alpha) {
   return sw;
 }
 
-// ------------------------------------------------------------------------------------------
-// launchers (template dispatch)
-// ------------------------------------------------------------------------------------------
-template <int T, bool A2, bool DBG>
-cudaError_t launch_small_t(const double2* psi, int N, int B, int gx, uint64_t a0, uint64_t count, const Alphas& al,
-                           double* partial, double* chi, cudaStream_t st) {
-  dim3 grid(gx, B);
-  return launch_counted(LK_SINGLE, st, [&] {
-    k_small<T, A2, DBG><<<grid, 256, 0, st>>>(psi, N, a0, count, al, partial, chi);
-    return cudaGetLastError();
-  });
-}
-
-template <bool A2, bool DBG>
-cudaError_t launch_small(int T, const double2* psi, int N, int B, int gx, uint64_t a0, uint64_t count, const Alphas& al,
-                         double* partial, double* chi, cudaStream_t st) {
-  switch (T) {
-#define C_(t) case t: return launch_small_t<t, A2, DBG>(psi, N, B, gx, a0, count, al, partial, chi, st);
-    C_(0) C_(1) C_(2) C_(3) C_(4) C_(5) C_(6) C_(7) C_(8) C_(9) C_(10)
-#undef C_
-  }
-  return cudaErrorInvalidValue;
-}
-
-constexpr int SMEM_128K = 2 * padded(32 * 256) * 8;  // 2 planes x (2^T + pad) x UPC units
-
-template <class K>
-cudaError_t set_smem(K kern, int bytes) {
-  return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-}
-
-template <int T, bool A2, bool DBG>
-cudaError_t launch_mid_t(const double2* psi, int N, int B, int gx, uint64_t a0, uint64_t count, const Alphas& al,
-                         double* partial, double* chi, cudaStream_t st) {
-  static bool init = false;
-  if (!init) {
-    cudaError_t e = set_smem(k_mid<T, A2, DBG>, SMEM_128K);
-    if (e != cudaSuccess) return e;
-    init = true;
-  }
-  dim3 grid(gx, B);
-  return launch_counted(LK_SINGLE, st, [&] {
-    k_mid<T, A2, DBG><<<grid, 256, SMEM_128K, st>>>(psi, N, a0, count, al, partial, chi);
-    return cudaGetLastError();
-  });
-}
-
-template <bool A2, bool DBG>
-cudaError_t launch_mid(int T, const double2* psi, int N, int B, int gx, uint64_t a0, uint64_t count, const Alphas& al,
-                       double* partial, double* chi, cudaStream_t st) {
-  switch (T) {
-    case 11: return launch_mid_t<11, A2, DBG>(psi, N, B, gx, a0, count, al, partial, chi, st);
-    case 12: return launch_mid_t<12, A2, DBG>(psi, N, B, gx, a0, count, al, partial, chi, st);
-    case 13: return launch_mid_t<13, A2, DBG>(psi, N, B, gx, a0, count, al, partial, chi, st);
-  }
-  return cudaErrorInvalidValue;
-}
-
-template <int L>
-cudaError_t launch_passA_t(const double2* psi, int N, uint64_t a0, int kcount, double* ws, int units, cudaStream_t st) {
-  static bool init = false;
-  if (!init) {
-    cudaError_t e = set_smem(k_passA<L>, SMEM_128K);
-    if (e != cudaSuccess) return e;
-    init = true;
-  }
-  const uint64_t items = (uint64_t)kcount << (N - 1 - L);
-  const unsigned grid = (unsigned)((items + units - 1) / units);
-  return launch_counted(LK_PASSA, st, [&] {
-    k_passA<L><<<grid, 256, SMEM_128K, st>>>(psi, N, a0, kcount, ws);
-    return cudaGetLastError();
-  });
-}
-
-cudaError_t launch_passA(const Plan& p, const double2* psi, uint64_t a0, int kcount, double* ws, cudaStream_t st) {
-  switch (p.L) {
-    case 10: return launch_passA_t<10>(psi, p.N, a0, kcount, ws, p.unitsA, st);
-    case 11: return launch_passA_t<11>(psi, p.N, a0, kcount, ws, p.unitsA, st);
-    case 12: return launch_passA_t<12>(psi, p.N, a0, kcount, ws, p.unitsA, st);
-    case 13: return launch_passA_t<13>(psi, p.N, a0, kcount, ws, p.unitsA, st);
-  }
-  return cudaErrorInvalidValue;
-}
-
-template <int TP, int CB, bool A2, bool DBG>
-cudaError_t launch_passB_t(const Plan& p, uint64_t a0, int kcount, const double* ws, const Alphas& al, double* partial,
-                           double* chi, cudaStream_t st) {
-  constexpr int BLK = TP >= 14 ? 512 : 256;
-  constexpr int SM = padded(BLK * 32) * 8;
-  static bool init = false;
-  if (!init) {
-    cudaError_t e = set_smem(k_passB<TP, CB, A2, DBG>, SM);
-    if (e != cudaSuccess) return e;
-    init = true;
-  }
-  const uint64_t items = (uint64_t)kcount * 2 * (1ull << (p.L - CB));
-  const unsigned grid = (unsigned)((items + p.unitsB - 1) / p.unitsB);
-  return launch_counted(LK_PASSB, st, [&] {
-    k_passB<TP, CB, A2, DBG><<<grid, BLK, SM, st>>>(p.N, p.L, a0, kcount, ws, al, partial, chi);
-    return cudaGetLastError();
-  });
-}
-
-template <bool A2, bool DBG>
-cudaError_t launch_passB(const Plan& p, uint64_t a0, int kcount, const double* ws, const Alphas& al, double* partial,
-                         double* chi, cudaStream_t st) {
-  const int key = p.TP * 16 + p.CB;
-  switch (key) {
-#define C_(tp, cb) case tp * 16 + cb: return launch_passB_t<tp, cb, A2, DBG>(p, a0, kcount, ws, al, partial, chi, st);
-    C_(10, 6) C_(11, 6) C_(12, 6) C_(13, 6) C_(13, 5) C_(13, 4) C_(13, 3) C_(13, 2) C_(14, 2)
-#undef C_
-  }
-  return cudaErrorInvalidValue;
-}
-
-template <int N>
-cudaError_t launch_passA10s_t(const Dev& d, const double2* psi, uint64_t a_first, int kcount, double* ws,
-                              cudaStream_t st) {
-  static bool init = false;
-  if (!init) {
-    cudaError_t e = set_smem(k_passA10s<N>, PA10_SMEM);
-    if (e != cudaSuccess) return e;
-    init = true;
-  }
-  const int groups = (kcount + 7) / 8;
-  const uint64_t items = (uint64_t)groups << (N - 11);
-  const unsigned grid = (unsigned)(items < (uint64_t)d.sms ? items : (uint64_t)d.sms);
-  return launch_counted(LK_PASSA, st, [&] {
-    k_passA10s<N><<<grid, 256, PA10_SMEM, st>>>(psi, a_first, kcount, groups, ws);
-    return cudaGetLastError();
-  });
-}
-
-template <int N>
-cudaError_t launch_passA_tmem_t(const Dev& d, const double2* psi, uint64_t a_first, int kcount, double* ws,
-                                cudaStream_t st) {
-  constexpr int L = N == 20 ? 11 : 10;
-  constexpr int SMEM = N == 20 ? PA11_SMEM : PA10_SMEM;
-  auto kern = [] { if constexpr (N == 20) return k_passA11t<20>; else return k_passA10s<N, true>; }();
-  static bool init = false;
-  if (!init) {
-    cudaError_t e = set_smem(kern, SMEM);
-    if (e != cudaSuccess) return e;
-    init = true;
-  }
-  const int groups = (kcount + 7) / 8;
-  const uint64_t items = (uint64_t)groups << (N - 1 - L);
-  const unsigned grid = (unsigned)(items < (uint64_t)d.sms ? items : (uint64_t)d.sms);
-  return launch_counted(LK_PASSA, st, [&] {
-    kern<<<grid, 256, SMEM, st>>>(psi, a_first, kcount, groups, ws);
-    return cudaGetLastError();
-  });
-}
-
-template <int N, bool A2>
-cudaError_t launch_passB_tmem_t(const Dev& d, int kcount, const double* ws, const Alphas& al, double* partial,
-                                cudaStream_t st) {
-  static bool init = false;
-  if (!init) {
-    cudaError_t e = set_smem(k_passBt8<N, A2>, PB8_SMEM);
-    if (e != cudaSuccess) return e;
-    init = true;
-  }
-  return launch_counted(LK_PASSB, st, [&] {
-    k_passBt8<N, A2><<<d.sms, 128, PB8_SMEM, st>>>(kcount, ws, al, partial);
-    return cudaGetLastError();
-  });
-}
-
-cudaError_t launch_tmem_pair(const Plan& p, const Dev& d, bool a2, const double2* psi, uint64_t a_first, int kcount,
-                             double* ws, const Alphas& al, double* partial, cudaStream_t st) {
-  cudaError_t e;
-  if (p.N == 20) {
-    e = launch_passA_tmem_t<20>(d, psi, a_first, kcount, ws, st);
-    if (e == cudaSuccess) e = a2 ? launch_passB_tmem_t<20, true>(d, kcount, ws, al, partial, st)
-                                 : launch_passB_tmem_t<20, false>(d, kcount, ws, al, partial, st);
-  } else {
-    e = launch_passA_tmem_t<19>(d, psi, a_first, kcount, ws, st);
-    if (e == cudaSuccess) e = a2 ? launch_passB_tmem_t<19, true>(d, kcount, ws, al, partial, st)
-                                 : launch_passB_tmem_t<19, false>(d, kcount, ws, al, partial, st);
-  }
-  return e;
-}
-
-template <int N, int L>
-cudaError_t launch_passAs_t(const Dev& d, const double2* psi, uint64_t a_first, int kcount, double* ws,
-                            cudaStream_t st) {
-  static bool init = false;
-  if (!init) {
-    cudaError_t e = set_smem(k_passAs<N, L>, pas_smem(L));
-    if (e != cudaSuccess) return e;
-    init = true;
-  }
-  const uint64_t units = (uint64_t)kcount << (N - 1 - L);
-  const uint64_t ctas = (units + (256 >> (L - 5)) - 1) / (256 >> (L - 5));
-  const unsigned grid = (unsigned)(ctas < (uint64_t)d.sms ? ctas : (uint64_t)d.sms);
-  return launch_counted(LK_PASSA, st, [&] {
-    k_passAs<N, L><<<grid, 256, pas_smem(L), st>>>(psi, a_first, kcount, ws);
-    return cudaGetLastError();
-  });
-}
-
-cudaError_t launch_passA10s(const Plan& p, const Dev& d, const double2* psi, uint64_t a_first, int kcount,
-                            double* ws, cudaStream_t st) {
-  switch (p.N) {
-    case 21: return launch_passAs_t<21, 12>(d, psi, a_first, kcount, ws, st);
-    case 22: return launch_passAs_t<22, 12>(d, psi, a_first, kcount, ws, st);
-    case 23: return launch_passAs_t<23, 12>(d, psi, a_first, kcount, ws, st);
-    case 24: return launch_passAs_t<24, 12>(d, psi, a_first, kcount, ws, st);
-    case 25: return launch_passAs_t<25, 13>(d, psi, a_first, kcount, ws, st);
-    case 15: return launch_passA10s_t<15>(d, psi, a_first, kcount, ws, st);
-    case 16: return launch_passA10s_t<16>(d, psi, a_first, kcount, ws, st);
-    case 17: return launch_passA10s_t<17>(d, psi, a_first, kcount, ws, st);
-    case 18: return launch_passA10s_t<18>(d, psi, a_first, kcount, ws, st);
-    case 19: return launch_passA10s_t<19>(d, psi, a_first, kcount, ws, st);
-    case 20: return launch_passA10s_t<20>(d, psi, a_first, kcount, ws, st);
-  }
-  return cudaErrorInvalidValue;
-}
-
 bool fused_enabled() {  // opt-in (SRE_FUSED=1): measured slower than the two staged launches
   const char* e = getenv("SRE_FUSED");
   return e && e[0] == '1';
-}
-
-template <int N, bool A2>
-cudaError_t launch_fused_t(const Dev& d, const double2* psi, uint64_t a_first, uint64_t count, double* ws,
-                           FusedCtl* ctl, const Alphas& al, double* partial, cudaStream_t st) {
-  static bool init = false;
-  if (!init) {
-    cudaError_t e = set_smem(k_fused<N, A2>, FZ_SMEM);
-    if (e != cudaSuccess) return e;
-    init = true;
-  }
-  cudaError_t e = cudaMemsetAsync(ctl, 0, sizeof(FusedCtl), st);
-  if (e != cudaSuccess) return e;
-  return launch_counted(LK_FUSED, st, [&] {
-    void* args[] = {(void*)&psi, (void*)&a_first, (void*)&count, (void*)&ws, (void*)&ctl, (void*)&al, (void*)&partial};
-    return cudaLaunchCooperativeKernel((const void*)k_fused<N, A2>, dim3(d.sms), dim3(256), args, FZ_SMEM, st);
-  });
-}
-
-template <bool A2>
-cudaError_t launch_fused(const Plan& p, const Dev& d, const double2* psi, uint64_t a_first, uint64_t count,
-                         double* ws, FusedCtl* ctl, const Alphas& al, double* partial, cudaStream_t st) {
-  switch (p.N) {
-#define C_(n) case n: return launch_fused_t<n, A2>(d, psi, a_first, count, ws, ctl, al, partial, st);
-    C_(15) C_(16) C_(17) C_(18) C_(19) C_(20)
-#undef C_
-  }
-  return cudaErrorInvalidValue;
-}
-
-template <int TP, int CB, bool A2>
-cudaError_t launch_passBt_t(const Plan& p, const Dev& d, int kcount, const double* ws, const Alphas& al,
-                            double* partial, cudaStream_t st) {
-  static bool init = false;
-  if (!init) {
-    cudaError_t e = set_smem(k_passBt<TP, CB, A2>, pbt_smem(TP));
-    if (e != cudaSuccess) return e;
-    init = true;
-  }
-  const unsigned grid = (unsigned)d.sms;
-  return launch_counted(LK_PASSB, st, [&] {
-    k_passBt<TP, CB, A2><<<grid, 256, pbt_smem(TP), st>>>(p.N, kcount, ws, al, partial);
-    return cudaGetLastError();
-  });
-}
-
-template <bool A2>
-cudaError_t launch_passBp(const Plan& p, const Dev& d, int kcount, const double* ws, const Alphas& al, double* partial,
-                          cudaStream_t st) {
-  if (p.N >= 21) {     // streamed path: tiles of 2^13 doubles, CB = 13 - H
-    switch (13 - p.H) {
-      case 7: return launch_passBt_t<13, 7, A2>(p, d, kcount, ws, al, partial, st);
-      case 6: return launch_passBt_t<13, 6, A2>(p, d, kcount, ws, al, partial, st);
-      case 5: return launch_passBt_t<13, 5, A2>(p, d, kcount, ws, al, partial, st);
-      case 4: return launch_passBt_t<13, 4, A2>(p, d, kcount, ws, al, partial, st);
-      case 3: return launch_passBt_t<13, 3, A2>(p, d, kcount, ws, al, partial, st);
-      case 2: return launch_passBt_t<13, 2, A2>(p, d, kcount, ws, al, partial, st);
-    }
-    return cudaErrorInvalidValue;
-  }
-  switch (12 - p.H) {  // slab-major tiles of 2^12 doubles: CB = 12 - H
-    case 8: return launch_passBt_t<12, 8, A2>(p, d, kcount, ws, al, partial, st);
-    case 7: return launch_passBt_t<12, 7, A2>(p, d, kcount, ws, al, partial, st);
-    case 6: return launch_passBt_t<12, 6, A2>(p, d, kcount, ws, al, partial, st);
-    case 5: return launch_passBt_t<12, 5, A2>(p, d, kcount, ws, al, partial, st);
-    case 4: return launch_passBt_t<12, 4, A2>(p, d, kcount, ws, al, partial, st);
-    case 3: return launch_passBt_t<12, 3, A2>(p, d, kcount, ws, al, partial, st);
-  }
-  return cudaErrorInvalidValue;
 }
 
 int occupancy_small(int T, const Dev& d) {
@@ -563,17 +234,13 @@ int occupancy_small(int T, const Dev& d) {
 // ------------------------------------------------------------------------------------------
 // the range driver: sums_dev[B][n_alpha+2] for a in [a_begin, a_end)
 // ------------------------------------------------------------------------------------------
-int run_range(const double2* psi, int N, int B, uint64_t a_begin, uint64_t a_end, const double* alpha, int n_alpha,
-              char* ws, size_t ws_bytes, double* sums_dev, cudaStream_t st) {
-  Dev d;
-  int rc = get_dev(d);
-  if (rc) return rc;
-  Plan p;
-  make_plan(N, d, p);
-  if (ws_bytes < ws_bytes_for(p, B)) return fail(SRE_EWORKSPACE, "workspace %zu < required %zu", ws_bytes, ws_bytes_for(p, B));
+// V = double: FP64 path; V = float: FP32 mode (psi already converted to complex64)
+template <class V>
+int run_range_t(const typename Cx<V>::T* psi, const Plan& p, const Dev& d, int N, int B, uint64_t a_begin,
+                uint64_t a_end, const double* alpha, int n_alpha, char* ws, double* sums_dev, cudaStream_t st) {
+  constexpr bool F64 = std::is_same<V, double>::value;
   double* partial = reinterpret_cast<double*>(ws);
-  const size_t partial_doubles = p.slots * NACC * (p.kind == TWOPASS ? 1 : (size_t)B);
-  double* slab = partial + partial_doubles;
+  V* slab = reinterpret_cast<V*>(ws + off_slab(p, B));
   FusedCtl* ctl = ctl_of(ws, p, B);
   CK(cudaMemsetAsync(ctl, 0, sizeof(FusedCtl), st));
   const uint64_t count = a_end - a_begin;
@@ -601,26 +268,26 @@ int run_range(const double2* psi, int N, int B, uint64_t a_begin, uint64_t a_end
       CK(cudaMemsetAsync(partial, 0, sizeof(double) * (size_t)gx * B * NACC, st));
       cudaError_t e;
       if (p.kind == SMALL)
-        e = sw.a2 ? launch_small<true, false>(p.T, psi, N, B, gx, a_begin, count, sw.al, partial, nullptr, st)
-                  : launch_small<false, false>(p.T, psi, N, B, gx, a_begin, count, sw.al, partial, nullptr, st);
+        e = sw.a2 ? launch_small<V, true, false>(p.T, psi, N, B, gx, a_begin, count, sw.al, partial, nullptr, st)
+                  : launch_small<V, false, false>(p.T, psi, N, B, gx, a_begin, count, sw.al, partial, nullptr, st);
       else
-        e = sw.a2 ? launch_mid<true, false>(p.T, psi, N, B, gx, a_begin, count, sw.al, partial, nullptr, st)
-                  : launch_mid<false, false>(p.T, psi, N, B, gx, a_begin, count, sw.al, partial, nullptr, st);
+        e = sw.a2 ? launch_mid<V, true, false>(p.T, psi, N, B, gx, a_begin, count, sw.al, partial, nullptr, st)
+                  : launch_mid<V, false, false>(p.T, psi, N, B, gx, a_begin, count, sw.al, partial, nullptr, st);
       if (e != cudaSuccess) return fail(SRE_ECUDA, "launch: %s", cudaGetErrorString(e));
       ra.nslots = gx;
       CK(launch_counted(LK_AUX, st, [&] { k_reduce<<<B, 256, 0, st>>>(partial, ra, sums_dev); return cudaGetLastError(); }));
     } else {
       for (int s = 0; s < B; ++s) {
-        const double2* ps = psi + ((size_t)s << N);
+        const typename Cx<V>::T* ps = psi + ((size_t)s << N);
         CK(cudaMemsetAsync(partial, 0, sizeof(double) * p.slots * NACC, st));
         // generic batches (a < 2^L, unaligned heads, L > 10): k_passA + k_passB
         auto generic = [&](uint64_t lo, uint64_t hi) -> int {
           for (uint64_t a = lo; a < hi; a += (uint64_t)p.K) {
             const int kc = (int)((hi - a) < (uint64_t)p.K ? (hi - a) : (uint64_t)p.K);
-            cudaError_t e = launch_passA(p, ps, a, kc, slab, st);
+            cudaError_t e = launch_passA<V>(p, ps, a, kc, slab, st);
             if (e != cudaSuccess) return fail(SRE_ECUDA, "passA: %s", cudaGetErrorString(e));
-            e = sw.a2 ? launch_passB<true, false>(p, a, kc, slab, sw.al, partial, nullptr, st)
-                      : launch_passB<false, false>(p, a, kc, slab, sw.al, partial, nullptr, st);
+            e = sw.a2 ? launch_passB<V, true, false>(p, a, kc, slab, sw.al, partial, nullptr, st)
+                      : launch_passB<V, false, false>(p, a, kc, slab, sw.al, partial, nullptr, st);
             if (e != cudaSuccess) return fail(SRE_ECUDA, "passB: %s", cudaGetErrorString(e));
           }
           return SRE_OK;
@@ -635,27 +302,29 @@ int run_range(const double2* psi, int N, int B, uint64_t a_begin, uint64_t a_end
           if (s0 > a_end) s0 = a_end;
           int rc2 = generic(a_begin, s0);
           if (rc2) return rc2;
-          if (fused_enabled() && p.L == 10 && s0 < a_end) {   // one persistent launch for the aligned bulk
-            cudaError_t e = sw.a2 ? launch_fused<true>(p, d, ps, s0, a_end - s0, slab, ctl, sw.al, partial, st)
-                                  : launch_fused<false>(p, d, ps, s0, a_end - s0, slab, ctl, sw.al, partial, st);
-            if (e != cudaSuccess) return fail(SRE_ECUDA, "fused: %s", cudaGetErrorString(e));
-            s0 = a_end;
-          }
           const uint64_t per = (uint64_t)8 * p.KG;
-          if (p.tmem) {
-            for (uint64_t a = s0; a < a_end; a += per) {
-              const int kc = (int)((a_end - a) < per ? (a_end - a) : per);
-              cudaError_t e = launch_tmem_pair(p, d, sw.a2, ps, a, kc, slab, sw.al, partial, st);
-              if (e != cudaSuccess) return fail(SRE_ECUDA, "tmem pair: %s", cudaGetErrorString(e));
+          if constexpr (F64) {   // FP64-only experimental paths
+            if (fused_enabled() && p.L == 10 && s0 < a_end) {   // one persistent launch for the aligned bulk
+              cudaError_t e = sw.a2 ? launch_fused<true>(p, d, ps, s0, a_end - s0, slab, ctl, sw.al, partial, st)
+                                    : launch_fused<false>(p, d, ps, s0, a_end - s0, slab, ctl, sw.al, partial, st);
+              if (e != cudaSuccess) return fail(SRE_ECUDA, "fused: %s", cudaGetErrorString(e));
+              s0 = a_end;
             }
-            s0 = a_end;
+            if (p.tmem) {
+              for (uint64_t a = s0; a < a_end; a += per) {
+                const int kc = (int)((a_end - a) < per ? (a_end - a) : per);
+                cudaError_t e = launch_tmem_pair(p, d, sw.a2, ps, a, kc, slab, sw.al, partial, st);
+                if (e != cudaSuccess) return fail(SRE_ECUDA, "tmem pair: %s", cudaGetErrorString(e));
+              }
+              s0 = a_end;
+            }
           }
           for (uint64_t a = s0; a < a_end; a += per) {
             const int kc = (int)((a_end - a) < per ? (a_end - a) : per);
-            cudaError_t e = launch_passA10s(p, d, ps, a, kc, slab, st);
+            cudaError_t e = launch_passA10s<V>(p, d, ps, a, kc, slab, st);
             if (e != cudaSuccess) return fail(SRE_ECUDA, "passA10s: %s", cudaGetErrorString(e));
-            e = sw.a2 ? launch_passBp<true>(p, d, kc, slab, sw.al, partial, st)
-                      : launch_passBp<false>(p, d, kc, slab, sw.al, partial, st);
+            e = sw.a2 ? launch_passBp<V, true>(p, d, kc, slab, sw.al, partial, st)
+                      : launch_passBp<V, false>(p, d, kc, slab, sw.al, partial, st);
             if (e != cudaSuccess) return fail(SRE_ECUDA, "passBp: %s", cudaGetErrorString(e));
           }
         }
@@ -668,6 +337,24 @@ int run_range(const double2* psi, int N, int B, uint64_t a_begin, uint64_t a_end
     }
   }
   return SRE_OK;
+}
+
+int run_range(const double2* psi, int N, int B, uint64_t a_begin, uint64_t a_end, const double* alpha, int n_alpha,
+              char* ws, size_t ws_bytes, double* sums_dev, cudaStream_t st, int prec = SRE_FP64) {
+  Dev d;
+  int rc = get_dev(d);
+  if (rc) return rc;
+  Plan p;
+  make_plan(N, d, p);
+  if (ws_bytes < ws_bytes_for(p, B, prec))
+    return fail(SRE_EWORKSPACE, "workspace %zu < required %zu", ws_bytes, ws_bytes_for(p, B, prec));
+  if (prec == SRE_FP32) {
+    float2* p32 = psi32_of(ws, p, B);
+    const uint64_t n = (uint64_t)B << N;
+    CK(launch_counted(LK_AUX, st, [&] { k_to_f32<<<4 * d.sms, 256, 0, st>>>(psi, p32, n); return cudaGetLastError(); }));
+    return run_range_t<float>(p32, p, d, N, B, a_begin, a_end, alpha, n_alpha, ws, sums_dev, st);
+  }
+  return run_range_t<double>(psi, p, d, N, B, a_begin, a_end, alpha, n_alpha, ws, sums_dev, st);
 }
 
 int validate_common(const void* psi, int N, int B, const double* alpha, int n_alpha) {
@@ -719,7 +406,9 @@ int cache_get(char** buf, size_t* have, size_t need) {
   return SRE_OK;
 }
 
-int exact_impl(const void* psi, int N, int B, const double* alpha, int n_alpha, double* out_M, double* out_ln) {
+int exact_impl(const void* psi, int N, int B, const double* alpha, int n_alpha, double* out_M, double* out_ln,
+               int prec = SRE_FP64) {
+  if (prec != SRE_FP64 && prec != SRE_FP32) return fail(SRE_EINVAL, "precision %d", prec);
   int rc = validate_common(psi, N, B, alpha, n_alpha);
   if (rc) return rc;
   if (!out_M) return fail(SRE_EINVAL, "out_M is NULL");
@@ -734,7 +423,7 @@ int exact_impl(const void* psi, int N, int B, const double* alpha, int n_alpha, 
   }
   Plan p;
   make_plan(N, d, p);
-  const size_t need = ws_bytes_for(p, B) + sizeof(double) * ((size_t)B * (n_alpha + 2) + (size_t)B);
+  const size_t need = ws_bytes_for(p, B, prec) + sizeof(double) * ((size_t)B * (n_alpha + 2) + (size_t)B);
   rc = cache_get(&g_cache.ws, &g_cache.ws_bytes, need);
   if (rc) return rc;
   cudaStream_t st = 0;
@@ -746,12 +435,11 @@ int exact_impl(const void* psi, int N, int B, const double* alpha, int n_alpha, 
     CK(cudaMemcpyAsync(g_cache.in, psi, psi_bytes, cudaMemcpyHostToDevice, st));
     dpsi = reinterpret_cast<const double2*>(g_cache.in);
   }
-  double* sums = reinterpret_cast<double*>(g_cache.ws + ws_bytes_for(p, B));
+  double* sums = reinterpret_cast<double*>(g_cache.ws + ws_bytes_for(p, B, prec));
   double* norms = sums + (size_t)B * (n_alpha + 2);
   // norm check (reading C6)
   {
-    double* part = reinterpret_cast<double*>(g_cache.ws) + p.slots * NACC * (p.kind == TWOPASS ? 1 : (size_t)B) +
-                   p.slab_doubles;  // the norm area of ws_bytes_for
+    double* part = reinterpret_cast<double*>(g_cache.ws + off_norm(p, B));  // the norm area
     const int nb = 64;
     dim3 g(nb, B);
     CK(launch_counted(LK_AUX, st, [&] { k_norm2_partial<<<g, 256, 0, st>>>(dpsi, N, part); return cudaGetLastError(); }));
@@ -762,7 +450,7 @@ int exact_impl(const void* psi, int N, int B, const double* alpha, int n_alpha, 
     for (int s = 0; s < B; ++s)
       if (!(std::fabs(hn[s] - 1.0) <= 1e-8)) return fail(SRE_ENOTNORM, "state %d: ||psi||^2 = %.17g", s, hn[s]);
   }
-  rc = run_range(dpsi, N, B, 0, 1ull << N, alpha, n_alpha, g_cache.ws, ws_bytes_for(p, B), sums, st);
+  rc = run_range(dpsi, N, B, 0, 1ull << N, alpha, n_alpha, g_cache.ws, ws_bytes_for(p, B, prec), sums, st, prec);
   if (rc) return rc;
   std::vector<double> hs((size_t)B * (n_alpha + 2));
   CK(cudaMemcpyAsync(hs.data(), sums, sizeof(double) * hs.size(), cudaMemcpyDeviceToHost, st));
@@ -813,6 +501,39 @@ int sre_exact_batched(const void* psi, int N, int B, const double* alpha, int n_
                       double* out_lost_norm) {
   g_err[0] = 0;
   return exact_impl(psi, N, B, alpha, n_alpha, out_M, out_lost_norm);
+}
+
+size_t sre_workspace_size_ex(int N, int B, int n_alpha, int precision) {
+  if (N < 1 || N > SRE_MAX_N || B < 1 || n_alpha < 1 || n_alpha > SRE_MAX_ALPHA) return 0;
+  if (precision != SRE_FP64 && precision != SRE_FP32) return 0;
+  Dev d;
+  Plan p;
+  make_plan(N, d, p);
+  return ws_bytes_for(p, B, precision);
+}
+
+int sre_exact_ex(const void* psi, int N, int B, const double* alpha, int n_alpha, int precision, double* out_M,
+                 double* out_lost_norm) {
+  g_err[0] = 0;
+  return exact_impl(psi, N, B, alpha, n_alpha, out_M, out_lost_norm, precision);
+}
+
+int sre_partial_sums_ex(const void* psi, int N, int B, uint64_t a_begin, uint64_t a_end, const double* alpha,
+                        int n_alpha, int precision, void* workspace, size_t ws_bytes, double* sums_dev, void* stream) {
+  g_err[0] = 0;
+  if (precision != SRE_FP64 && precision != SRE_FP32) return fail(SRE_EINVAL, "precision %d", precision);
+  int rc = validate_common(psi, N, B, alpha, n_alpha);
+  if (rc) return rc;
+  if (!workspace) return fail(SRE_EINVAL, "workspace is NULL");
+  if (!sums_dev) return fail(SRE_EINVAL, "sums_dev is NULL");
+  if (a_begin > a_end || a_end > (1ull << N)) return fail(SRE_ERANGE, "range [%llu, %llu) outside [0, 2^%d]",
+                                                          (unsigned long long)a_begin, (unsigned long long)a_end, N);
+  bool dv = false;
+  is_device_ptr(psi, dv);
+  if (!dv) return fail(SRE_EINVAL, "psi must be a device pointer");
+  return run_range(reinterpret_cast<const double2*>(psi), N, B, a_begin, a_end, alpha, n_alpha,
+                   reinterpret_cast<char*>(workspace), ws_bytes, sums_dev, reinterpret_cast<cudaStream_t>(stream),
+                   precision);
 }
 
 int sre_partial_sums(const void* psi, int N, int B, uint64_t a_begin, uint64_t a_end, const double* alpha, int n_alpha,
@@ -884,17 +605,17 @@ int sre_chi(const void* psi, int N, uint64_t a, double* chi_dev, void* stream) {
   al.n = 1;
   cudaError_t e = cudaSuccess;
   if (p.kind == SMALL) {
-    e = launch_small<false, true>(p.T, dpsi, N, 1, 1, a, 1, al, nullptr, chi_dev, st);
+    e = launch_small<double, false, true>(p.T, dpsi, N, 1, 1, a, 1, al, nullptr, chi_dev, st);
   } else if (p.kind == MID) {
-    e = launch_mid<false, true>(p.T, dpsi, N, 1, 1, a, 1, al, nullptr, chi_dev, st);
+    e = launch_mid<double, false, true>(p.T, dpsi, N, 1, 1, a, 1, al, nullptr, chi_dev, st);
   } else {
     std::lock_guard<std::mutex> lk(g_cache.mu);
     if (g_cache.dev != d.id) { g_cache.ws = nullptr; g_cache.ws_bytes = 0; g_cache.in = nullptr; g_cache.in_bytes = 0; g_cache.dev = d.id; }
     rc = cache_get(&g_cache.ws, &g_cache.ws_bytes, ws_bytes_for(p, 1));
     if (rc) return rc;
-    double* slab = reinterpret_cast<double*>(g_cache.ws) + p.slots * NACC;
-    e = launch_passA(p, dpsi, a, 1, slab, st);
-    if (e == cudaSuccess) e = launch_passB<false, true>(p, a, 1, slab, al, nullptr, chi_dev, st);
+    double* slab = reinterpret_cast<double*>(g_cache.ws + off_slab(p, 1));
+    e = launch_passA<double>(p, dpsi, a, 1, slab, st);
+    if (e == cudaSuccess) e = launch_passB<double, false, true>(p, a, 1, slab, al, nullptr, chi_dev, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   }
   if (e != cudaSuccess) return fail(SRE_ECUDA, "sre_chi: %s", cudaGetErrorString(e));

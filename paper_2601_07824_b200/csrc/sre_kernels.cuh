@@ -37,6 +37,12 @@ struct Alphas {
   double alpha[MAXA];
 };
 
+// value type of a precision: FP64 (default) or FP32 mode (transform/workspace in FP32,
+// accumulators FP64; north-star "optional FP32 mode", tolerance 1e-4)
+template <class R> struct Cx;
+template <> struct Cx<double> { using T = double2; };
+template <> struct Cx<float> { using T = float2; };
+
 // ------------------------------------------------------------------------------------------
 // small helpers
 // ------------------------------------------------------------------------------------------
@@ -69,15 +75,15 @@ __host__ __device__ constexpr Round round_k(int T, int LO, int k) {
   }
 }
 
-template <int RLO, int RHI>
-__device__ __forceinline__ void bfly32(double (&v)[32]) {
+template <int RLO, int RHI, class R>
+__device__ __forceinline__ void bfly32(R (&v)[32]) {
 #pragma unroll
   for (int b = RLO; b < RHI; ++b) {
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
       if ((i >> b) & 1) continue;
       const int k = i | (1 << b);
-      const double u = v[i], w = v[k];
+      const R u = v[i], w = v[k];
       v[i] = u + w;
       v[k] = u - w;
     }
@@ -96,10 +102,10 @@ struct BarCta { __device__ __forceinline__ void sync() const { __syncthreads(); 
 // Rounds K..end of the transform of NP planes (each a 2^T vector in its own 2^T smem slice).
 // On entry the registers hold round K-1's layout (or round 0's with butterflies pending if
 // K == 0); on exit the final round's layout with all butterflies done.
-template <int T, int LO, int K, int NP, class Bar, bool SEQ = false>
+template <int T, int LO, int K, int NP, class Bar, bool SEQ = false, class R = double>
 struct Rounds {
   // SEQ: the NP planes share one 2^T smem slice and are exchanged one after the other.
-  __device__ __forceinline__ static void run(double (&v)[NP][32], double* sm, uint32_t t, const Bar& bar) {
+  __device__ __forceinline__ static void run(R (&v)[NP][32], R* sm, uint32_t t, const Bar& bar) {
     constexpr int NR = nrounds(T, LO);
     if constexpr (K < NR) {
       constexpr Round r = round_k(T, LO, K);
@@ -130,7 +136,7 @@ struct Rounds {
       }
 #pragma unroll
       for (int pl = 0; pl < NP; ++pl) bfly32<r.rlo, r.rhi>(v[pl]);
-      Rounds<T, LO, K + 1, NP, Bar, SEQ>::run(v, sm, t, bar);
+      Rounds<T, LO, K + 1, NP, Bar, SEQ, R>::run(v, sm, t, bar);
     }
   }
 };
@@ -140,10 +146,10 @@ __host__ __device__ constexpr int final_s() { return round_k(T, LO, nrounds(T, L
 // ------------------------------------------------------------------------------------------
 // epilogue: power sums of t' = y^2 (DESIGN "Epilogue"); A2 = compile-time single alpha == 2
 // ------------------------------------------------------------------------------------------
-template <bool A2>
+template <bool A2, class R = double>
 struct Epi {
-  __device__ __forceinline__ static void add(double (&acc)[NACC], double y, const Alphas& al) {
-    const double t = y * y;
+  __device__ __forceinline__ static void add(R (&acc)[NACC], R y, const Alphas& al) {
+    const R t = y * y;
     acc[MAXA] += t;
     if constexpr (A2) {
       acc[0] = fma(t, t, acc[0]);
@@ -152,30 +158,30 @@ struct Epi {
       for (int i = 0; i < MAXA; ++i) {
         if (i < al.n) {
           if (al.kind[i] == 0) {
-            double pw = t;
+            R pw = t;
             for (int k = 1; k < al.iexp[i]; ++k) pw *= t;
             acc[i] += pw;
           } else {
-            acc[i] += (t > 0.0) ? exp(al.alpha[i] * log(t)) : 0.0;
+            acc[i] += (t > R(0)) ? exp(R(al.alpha[i]) * log(t)) : R(0);
           }
         }
       }
-      if (al.need_log) acc[MAXA + 1] += (t > 0.0) ? t * log(t) : 0.0;
+      if (al.need_log) acc[MAXA + 1] += (t > R(0)) ? t * log(t) : R(0);
     }
   }
 };
 
 // Epilogue of one tile's 32 values per thread into a fresh local sum, then one add into the
 // long-lived accumulators: keeps the running-sum chains ~32x shorter (DESIGN "Summation").
-template <bool A2>
-__device__ __forceinline__ void tile_accumulate(double (&acc)[NACC], const double (&v)[32], const Alphas& al) {
-  double loc[NACC];
+template <bool A2, class R>
+__device__ __forceinline__ void tile_accumulate(double (&acc)[NACC], const R (&v)[32], const Alphas& al) {
+  R loc[NACC];          // FP32 mode: 32-term local sums in FP32, one conversion per tile
 #pragma unroll
-  for (int i = 0; i < NACC; ++i) loc[i] = 0.0;
+  for (int i = 0; i < NACC; ++i) loc[i] = R(0);
 #pragma unroll
-  for (int j = 0; j < 32; ++j) Epi<A2>::add(loc, v[j], al);
+  for (int j = 0; j < 32; ++j) Epi<A2, R>::add(loc, v[j], al);
 #pragma unroll
-  for (int i = 0; i < NACC; ++i) acc[i] += loc[i];
+  for (int i = 0; i < NACC; ++i) acc[i] += (double)loc[i];
 }
 
 // Block reduction of the NACC accumulators; thread 0 adds them to partial[slot].
@@ -202,20 +208,22 @@ __device__ __forceinline__ void block_flush(double (&acc)[NACC], double* partial
 }
 
 // Generation of (A_y, B_y) for the half-index y of X-string a (pivot p; a == 0 special).
-__device__ __forceinline__ void gen_pair(const double2* __restrict__ psi, uint64_t y, uint64_t a, int p,
-                                         int N, double& A, double& B) {
+template <class R>
+__device__ __forceinline__ void gen_pair(const typename Cx<R>::T* __restrict__ psi, uint64_t y, uint64_t a, int p,
+                                         int N, R& A, R& B) {
+  using C2 = typename Cx<R>::T;
   if (a != 0) {
     const uint64_t x = ins0(y, p);
-    const double2 q = __ldg(psi + x);        // alpha_x = psi_x
-    const double2 r = __ldg(psi + (x ^ a));  // beta_x = psi_{x^a}
+    const C2 q = __ldg(psi + x);             // alpha_x = psi_x
+    const C2 r = __ldg(psi + (x ^ a));       // beta_x = psi_{x^a}
     A = fma(r.x, q.x, r.y * q.y);            // Re conj(beta) alpha
     B = fma(r.x, q.y, -(r.y * q.x));         // Im conj(beta) alpha
   } else {
     const uint64_t x0 = y, x1 = y | (1ull << (N - 1));
-    const double2 q0 = __ldg(psi + x0), q1 = __ldg(psi + x1);
-    const double n0 = fma(q0.x, q0.x, q0.y * q0.y), n1 = fma(q1.x, q1.x, q1.y * q1.y);
-    A = (n0 + n1) * 0.5;
-    B = (n0 - n1) * 0.5;
+    const C2 q0 = __ldg(psi + x0), q1 = __ldg(psi + x1);
+    const R n0 = fma(q0.x, q0.x, q0.y * q0.y), n1 = fma(q1.x, q1.x, q1.y * q1.y);
+    A = (n0 + n1) * R(0.5);
+    B = (n0 - n1) * R(0.5);
   }
 }
 __device__ __forceinline__ int pivot_of(uint64_t a, int N) { return a ? 63 - __clzll((long long)a) : N - 1; }
@@ -241,14 +249,14 @@ __device__ __forceinline__ void chi_store(double* chi, uint64_t a, int p, int pl
 // k_small: T = N-1 <= 10.  Group of G = min(32, 2^T) lanes per X-string, R = 2^T/G values
 // per plane per lane; register bits then shuffle bits.  One pass, no workspace.
 // ------------------------------------------------------------------------------------------
-template <int T, bool A2, bool DEBUG>
-__global__ void __launch_bounds__(256) k_small(const double2* __restrict__ psi_all, int N, uint64_t a0,
+template <int T, bool A2, bool DEBUG, class V = double>
+__global__ void __launch_bounds__(256) k_small(const typename Cx<V>::T* __restrict__ psi_all, int N, uint64_t a0,
                                                uint64_t count, Alphas al, double* partial, double* chi) {
   constexpr int G = T >= 5 ? 32 : (1 << T);
   constexpr int LG = T >= 5 ? 5 : T;
   constexpr int R = (1 << T) / G;
   constexpr int PER_CTA = 256 / G;
-  const double2* psi = psi_all + ((size_t)blockIdx.y << N);
+  const typename Cx<V>::T* psi = psi_all + ((size_t)blockIdx.y << N);
   const int g = threadIdx.x & (G - 1);
   double acc[NACC];
 #pragma unroll
@@ -260,18 +268,18 @@ __global__ void __launch_bounds__(256) k_small(const double2* __restrict__ psi_a
     const bool valid = item < count;
     const uint64_t a = a0 + item;
     const int p = pivot_of(a, N);
-    double A[R], B[R];
+    V A[R], B[R];
 #pragma unroll
     for (int j = 0; j < R; ++j) {
-      A[j] = 0.0; B[j] = 0.0;
-      if (valid) gen_pair(psi, (uint64_t)g + (uint64_t)G * j, a, p, N, A[j], B[j]);
+      A[j] = V(0); B[j] = V(0);
+      if (valid) gen_pair<V>(psi, (uint64_t)g + (uint64_t)G * j, a, p, N, A[j], B[j]);
     }
 #pragma unroll
     for (int h = 1; h < R; h <<= 1)
 #pragma unroll
       for (int i = 0; i < R; ++i) {
         if (i & h) continue;
-        double u = A[i], w = A[i + h]; A[i] = u + w; A[i + h] = u - w;
+        V u = A[i], w = A[i + h]; A[i] = u + w; A[i + h] = u - w;
         u = B[i]; w = B[i + h]; B[i] = u + w; B[i + h] = u - w;
       }
 #pragma unroll
@@ -279,8 +287,8 @@ __global__ void __launch_bounds__(256) k_small(const double2* __restrict__ psi_a
       const bool up = (g & m) != 0;
 #pragma unroll
       for (int i = 0; i < R; ++i) {
-        const double pa = __shfl_xor_sync(0xffffffffu, A[i], m, G);
-        const double pb = __shfl_xor_sync(0xffffffffu, B[i], m, G);
+        const V pa = __shfl_xor_sync(0xffffffffu, A[i], m, G);
+        const V pb = __shfl_xor_sync(0xffffffffu, B[i], m, G);
         A[i] = up ? pa - A[i] : A[i] + pa;
         B[i] = up ? pb - B[i] : B[i] + pb;
       }
@@ -294,7 +302,7 @@ __global__ void __launch_bounds__(256) k_small(const double2* __restrict__ psi_a
         }
       } else {
 #pragma unroll
-        for (int j = 0; j < R; ++j) { Epi<A2>::add(acc, A[j], al); Epi<A2>::add(acc, B[j], al); }
+        for (int j = 0; j < R; ++j) { Epi<A2>::add(acc, (double)A[j], al); Epi<A2>::add(acc, (double)B[j], al); }
       }
     }
   }
@@ -305,12 +313,12 @@ __global__ void __launch_bounds__(256) k_small(const double2* __restrict__ psi_a
 // k_mid: 11 <= T = N-1 <= 13.  A unit of NT = 2^(T-5) threads owns one X-string: 32 values of
 // each plane per thread, smem 2 * 2^T doubles per unit.  CTA = 256 threads.
 // ------------------------------------------------------------------------------------------
-template <int T>
-__device__ __forceinline__ void unit_gen(const double2* __restrict__ psi, uint64_t ybase, uint64_t a, int p, int N,
-                                         uint32_t t, double (&v)[2][32]) {
+template <int T, class V>
+__device__ __forceinline__ void unit_gen(const typename Cx<V>::T* __restrict__ psi, uint64_t ybase, uint64_t a, int p,
+                                         int N, uint32_t t, V (&v)[2][32]) {
   constexpr int NT = 1 << (T - 5);
 #pragma unroll
-  for (int j = 0; j < 32; ++j) gen_pair(psi, ybase + t + (uint64_t)NT * j, a, p, N, v[0][j], v[1][j]);
+  for (int j = 0; j < 32; ++j) gen_pair<V>(psi, ybase + t + (uint64_t)NT * j, a, p, N, v[0][j], v[1][j]);
 }
 
 template <int T, class F>
@@ -320,25 +328,25 @@ __device__ __forceinline__ void with_unit_bar(F&& f) {
   else f(BarNamed{1 + (int)(threadIdx.x / NT), NT});
 }
 
-template <int T, bool A2, bool DEBUG>
-__global__ void __launch_bounds__(256, 1) k_mid(const double2* __restrict__ psi_all, int N, uint64_t a0,
+template <int T, bool A2, bool DEBUG, class V = double>
+__global__ void __launch_bounds__(256, 1) k_mid(const typename Cx<V>::T* __restrict__ psi_all, int N, uint64_t a0,
                                                 uint64_t count, Alphas al, double* partial, double* chi) {
   constexpr int NT = 1 << (T - 5);
   constexpr int UPC = 256 / NT;
   extern __shared__ double smem[];
-  const double2* psi = psi_all + ((size_t)blockIdx.y << N);
+  const typename Cx<V>::T* psi = psi_all + ((size_t)blockIdx.y << N);
   const uint32_t t = threadIdx.x & (NT - 1);
   const int unit = threadIdx.x / NT;
-  double* sm = smem + (size_t)unit * 2 * padded(1 << T);
+  V* sm = reinterpret_cast<V*>(smem + (size_t)unit * 2 * padded(1 << T));
   double acc[NACC];
 #pragma unroll
   for (int i = 0; i < NACC; ++i) acc[i] = 0.0;
   for (uint64_t item = (uint64_t)blockIdx.x * UPC + unit; item < count; item += (uint64_t)gridDim.x * UPC) {
     const uint64_t a = a0 + item;
     const int p = pivot_of(a, N);
-    double v[2][32];
-    unit_gen<T>(psi, 0, a, p, N, t, v);
-    with_unit_bar<T>([&](const auto& bar) { Rounds<T, 0, 0, 2, std::decay_t<decltype(bar)>>::run(v, sm, t, bar); });
+    V v[2][32];
+    unit_gen<T, V>(psi, 0, a, p, N, t, v);
+    with_unit_bar<T>([&](const auto& bar) { Rounds<T, 0, 0, 2, std::decay_t<decltype(bar)>, false, V>::run(v, sm, t, bar); });
     if constexpr (DEBUG) {
       constexpr int sf = final_s<T, 0>();
 #pragma unroll
@@ -359,16 +367,16 @@ __global__ void __launch_bounds__(256, 1) k_mid(const double2* __restrict__ psi_
 // Pass A: a unit (NT = 2^(L-5) threads) generates one row y_h of both planes and transforms
 // the L low bits; writes row positions pos = t + NT*j (position pos holds b_l = lay(t,j,sL)).
 // ------------------------------------------------------------------------------------------
-template <int L>
-__global__ void __launch_bounds__(256, 1) k_passA(const double2* __restrict__ psi, int N, uint64_t a0,
-                                                  int kcount, double* __restrict__ ws) {
+template <int L, class V = double>
+__global__ void __launch_bounds__(256, 1) k_passA(const typename Cx<V>::T* __restrict__ psi, int N, uint64_t a0,
+                                                  int kcount, V* __restrict__ ws) {
   constexpr int NT = 1 << (L - 5);
   constexpr int UPC = 256 / NT;
   extern __shared__ double smem[];
   const int H = N - 1 - L;
   const uint32_t t = threadIdx.x & (NT - 1);
   const int unit = threadIdx.x / NT;
-  double* sm = smem + (size_t)unit * 2 * padded(1 << L);
+  V* sm = reinterpret_cast<V*>(smem + (size_t)unit * 2 * padded(1 << L));
   // item = y_h * kcount + k: the X-strings of the batch (which share a_h) take the same psi rows
   // at the same time, so each row pair comes from HBM once per batch and from L2 otherwise
   const uint64_t item = (uint64_t)blockIdx.x * UPC + unit;
@@ -378,11 +386,11 @@ __global__ void __launch_bounds__(256, 1) k_passA(const double2* __restrict__ ps
   const uint64_t yh = item / (uint64_t)kcount;
   const uint64_t a = a0 + (uint64_t)k;
   const int p = pivot_of(a, N);
-  double v[2][32];
-  unit_gen<L>(psi, yh << L, a, p, N, t, v);
-  with_unit_bar<L>([&](const auto& bar) { Rounds<L, 0, 0, 2, std::decay_t<decltype(bar)>>::run(v, sm, t, bar); });
+  V v[2][32];
+  unit_gen<L, V>(psi, yh << L, a, p, N, t, v);
+  with_unit_bar<L>([&](const auto& bar) { Rounds<L, 0, 0, 2, std::decay_t<decltype(bar)>, false, V>::run(v, sm, t, bar); });
   const size_t plane = (size_t)1 << (N - 1);
-  double* w0 = ws + (size_t)k * 2 * plane + (yh << L) + t;
+  V* w0 = ws + (size_t)k * 2 * plane + (yh << L) + t;
 #pragma unroll
   for (int j = 0; j < 32; ++j) {
     __stcg(w0 + (size_t)NT * j, v[0][j]);
@@ -392,9 +400,9 @@ __global__ void __launch_bounds__(256, 1) k_passA(const double2* __restrict__ ps
 
 // Pass B: a unit (NT = 2^(TP-5) threads, TP = CB + H) reads a slab of C = 2^CB columns x 2^H
 // rows of one plane, transforms the H row bits, and accumulates the epilogue.
-template <int TP, int CB, bool A2, bool DEBUG>
+template <int TP, int CB, bool A2, bool DEBUG, class V = double>
 __global__ void __launch_bounds__(TP >= 14 ? 512 : 256, 1) k_passB(int N, int L, uint64_t a0, int kcount,
-                                                                   const double* __restrict__ ws, Alphas al,
+                                                                   const V* __restrict__ ws, Alphas al,
                                                                    double* partial, double* chi) {
   constexpr int NT = 1 << (TP - 5);
   constexpr int BLK = TP >= 14 ? 512 : 256;
@@ -403,7 +411,7 @@ __global__ void __launch_bounds__(TP >= 14 ? 512 : 256, 1) k_passB(int N, int L,
   extern __shared__ double smem[];
   const uint32_t t = threadIdx.x & (NT - 1);
   const int unit = threadIdx.x / NT;
-  double* sm = smem + (size_t)unit * padded(1 << TP);
+  V* sm = reinterpret_cast<V*>(smem + (size_t)unit * padded(1 << TP));
   double acc[NACC];
 #pragma unroll
   for (int i = 0; i < NACC; ++i) acc[i] = 0.0;
@@ -412,14 +420,14 @@ __global__ void __launch_bounds__(TP >= 14 ? 512 : 256, 1) k_passB(int N, int L,
   if (item < (uint64_t)kcount * 2 * slabs) {
     const uint64_t kp = item / slabs, slab = item % slabs;
     const size_t plane_sz = (size_t)1 << (N - 1);
-    const double* src = ws + kp * plane_sz + (slab << CB);
-    double v[1][32];
+    const V* src = ws + kp * plane_sz + (slab << CB);
+    V v[1][32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       const uint32_t e = t + (uint32_t)NT * j;  // round-0 layout
       v[0][j] = __ldcg(src + ((size_t)(e >> CB) << L) + (e & ((1u << CB) - 1u)));
     }
-    with_unit_bar<TP>([&](const auto& bar) { Rounds<TP, CB, 0, 1, std::decay_t<decltype(bar)>>::run(v, sm, t, bar); });
+    with_unit_bar<TP>([&](const auto& bar) { Rounds<TP, CB, 0, 1, std::decay_t<decltype(bar)>, false, V>::run(v, sm, t, bar); });
     if constexpr (DEBUG) {
       const uint64_t a = a0 + kp / 2;
       const int p = pivot_of(a, N);
@@ -496,13 +504,14 @@ constexpr int PA10_SMEM = PA10_NS * 2 * 1024 * 16 + 8 * padded(1024) * 8;  // 12
 // finish with a ring slot refills it with the item NS positions ahead.  Warp w generates
 // X-string 8g + w from the staged rows, transforms 10 bits (one warp-local exchange per
 // plane) and writes its row of both planes.
-template <int N, bool RM = false>   // RM: row-major workspace for the TMEM pass B (pos = lane + 32 j)
-__global__ void __launch_bounds__(256, 1) k_passA10s(const double2* __restrict__ psi, uint64_t a_first,
-                                                     int kcount, int groups, double* __restrict__ ws) {
-  constexpr int cb = RM ? 10 : 12 - (N - 11);                   // pass B tile = 2^12 doubles
+template <int N, bool RM = false, class V = double>   // RM: chunk-major workspace for the TMEM pass B
+__global__ void __launch_bounds__(256, 1) k_passA10s(const typename Cx<V>::T* __restrict__ psi, uint64_t a_first,
+                                                     int kcount, int groups, V* __restrict__ ws) {
+  using C2 = typename Cx<V>::T;
+  constexpr int cb = RM ? 10 : 12 - (N - 11);                   // pass B tile = 2^12 values
   extern __shared__ __align__(128) double smem[];
-  double2* ring = reinterpret_cast<double2*>(smem);             // [NS][q row | r row][1024]
-  double* exch = smem + PA10_NS * 2 * 1024 * 2;                 // [warp][padded 1024]
+  C2* ring = reinterpret_cast<C2*>(smem);                       // [NS][q row | r row][1024]
+  V* exch = reinterpret_cast<V*>(smem + PA10_NS * 2 * 1024 * 2);   // [warp][padded 1024]
   __shared__ __align__(8) uint64_t full[PA10_NS];
   __shared__ int used[PA10_NS];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -515,10 +524,10 @@ __global__ void __launch_bounds__(256, 1) k_passA10s(const double2* __restrict__
     const uint64_t ag = a_first + 8 * g;
     const int p = 63 - __clzll((long long)ag);
     const uint64_t xh = ins0(yh, p - 10);
-    double2* dst = ring + (size_t)slot * 2048;
-    mbar_expect_tx(&full[slot], 2 * 1024 * 16);
-    bulk_g2s(dst, psi + (xh << 10), 1024 * 16, &full[slot]);
-    bulk_g2s(dst + 1024, psi + ((xh ^ (ag >> 10)) << 10), 1024 * 16, &full[slot]);
+    C2* dst = ring + (size_t)slot * 2048;
+    mbar_expect_tx(&full[slot], 2 * 1024 * sizeof(C2));
+    bulk_g2s(dst, psi + (xh << 10), 1024 * sizeof(C2), &full[slot]);
+    bulk_g2s(dst + 1024, psi + ((xh ^ (ag >> 10)) << 10), 1024 * sizeof(C2), &full[slot]);
   };
   if (threadIdx.x == 0) {
     for (int i = 0; i < PA10_NS; ++i) { mbar_init(&full[i], 1); used[i] = 0; }
@@ -528,23 +537,23 @@ __global__ void __launch_bounds__(256, 1) k_passA10s(const double2* __restrict__
   if (threadIdx.x == 0)
     for (int i = 0; i < PA10_NS; ++i)
       if (blockIdx.x + (uint64_t)i * gridDim.x < items) issue(blockIdx.x + (uint64_t)i * gridDim.x, i);
-  double* xw = exch + (size_t)w * padded(1024);
+  V* xw = exch + (size_t)w * padded(1024);
   uint32_t n = 0;
   for (uint64_t item = blockIdx.x; item < items; item += gridDim.x, ++n) {
     const int slot = (int)(n % PA10_NS);
     mbar_wait(&full[slot], (n / PA10_NS) & 1u);
     const uint64_t g = item >> H, yh = item & (rows - 1);
     const int k = 8 * (int)g + w;
-    const double2* sq = ring + (size_t)slot * 2048;
-    double v[2][32];
+    const C2* sq = ring + (size_t)slot * 2048;
+    V v[2][32];
     const bool active = k < kcount;
     if (active) {
       const uint32_t al = (uint32_t)((a_first + (uint64_t)k) & 1023u);
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
         const uint32_t yl = lane + 32 * j;
-        const double2 q = sq[yl];
-        const double2 r = sq[1024 + (yl ^ al)];
+        const C2 q = sq[yl];
+        const C2 r = sq[1024 + (yl ^ al)];
         v[0][j] = fma(r.x, q.x, r.y * q.y);
         v[1][j] = fma(r.x, q.y, -(r.y * q.x));
       }
@@ -560,12 +569,12 @@ __global__ void __launch_bounds__(256, 1) k_passA10s(const double2* __restrict__
       }
     }
     if (active) {
-      Rounds<10, 0, 0, 2, BarWarp, true>::run(v, xw, lane, BarWarp{});
+      Rounds<10, 0, 0, 2, BarWarp, true, V>::run(v, xw, lane, BarWarp{});
       // slab-major workspace: (y_h, pos) -> ((pos >> cb) << (H + cb)) | (y_h << cb) | (pos & (C-1));
       // RM (TMEM pass B, H = 8): chunk-major ((pos >> 7) << 15) + row_off(y_h) + (pos & 127)
       if constexpr (RM) {
         static_assert(H == 8, "chunk-major layout assumes H = 8");
-        double* w1 = ws + (size_t)k * 2 * plane + cm_row_off(yh) + lane;
+        V* w1 = ws + (size_t)k * 2 * plane + cm_row_off(yh) + lane;
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const size_t o = ((size_t)(j >> 2) << 15) + 32 * (j & 3);
@@ -574,7 +583,7 @@ __global__ void __launch_bounds__(256, 1) k_passA10s(const double2* __restrict__
         }
         continue;
       }
-      double* w0 = ws + (size_t)k * 2 * plane + (yh << cb);
+      V* w0 = ws + (size_t)k * 2 * plane + (yh << cb);
       constexpr uint32_t cm = (1u << cb) - 1u;
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
@@ -596,8 +605,8 @@ constexpr int PBT_NS = 3;
 __host__ __device__ constexpr int pbt_slot(int TP) { return padded(1 << TP); }         // tile + exchange padding
 __host__ __device__ constexpr int pbt_smem(int TP) { return PBT_NS * 256 / (1 << (TP - 5)) * pbt_slot(TP) * 8; }
 
-template <int TP, int CB, bool A2>   // TP = 12: two 128-thread units; TP = 13: one 256-thread unit
-__global__ void __launch_bounds__(256, 1) k_passBt(int N, int kcount, const double* __restrict__ ws, Alphas al,
+template <int TP, int CB, bool A2, class V = double>   // TP = 12: two 128-thread units; 13: one 256-thread unit
+__global__ void __launch_bounds__(256, 1) k_passBt(int N, int kcount, const V* __restrict__ ws, Alphas al,
                                                    double* partial) {
   constexpr int NT = 1 << (TP - 5), UNITS = 256 / NT, TILE = 1 << TP, SLOT = pbt_slot(TP);
   extern __shared__ __align__(128) double smem[];
@@ -607,7 +616,7 @@ __global__ void __launch_bounds__(256, 1) k_passBt(int N, int kcount, const doub
   const int L = N - 1 - (TP - CB);
   const uint64_t slabs = 1ull << (L - CB);
   const uint64_t tiles = (uint64_t)kcount * 2 * slabs;   // tile = kp * slabs + slab, contiguous blocks
-  double* ring = smem + (size_t)unit * PBT_NS * SLOT;
+  V* ring = reinterpret_cast<V*>(smem + (size_t)unit * PBT_NS * SLOT);   // slots of SLOT doubles
   const BarNamed bar{1 + unit, NT};
   if (threadIdx.x == 0) {
     for (int u = 0; u < UNITS; ++u)
@@ -616,9 +625,10 @@ __global__ void __launch_bounds__(256, 1) k_passBt(int N, int kcount, const doub
   }
   __syncthreads();
   const uint64_t first = (uint64_t)blockIdx.x * UNITS + unit, step = (uint64_t)gridDim.x * UNITS;
+  constexpr int SLOT_V = SLOT * (int)(sizeof(double) / sizeof(V));      // slot stride in V elements
   auto issue = [&](uint64_t tile, int slot) {
-    mbar_expect_tx(&full[unit][slot], TILE * 8);
-    bulk_g2s(ring + (size_t)slot * SLOT, ws + tile * TILE, TILE * 8, &full[unit][slot]);
+    mbar_expect_tx(&full[unit][slot], TILE * sizeof(V));
+    bulk_g2s(ring + (size_t)slot * SLOT_V, ws + tile * TILE, TILE * sizeof(V), &full[unit][slot]);
   };
   if (t == 0)
     for (int i = 0; i < PBT_NS; ++i)
@@ -629,12 +639,12 @@ __global__ void __launch_bounds__(256, 1) k_passBt(int N, int kcount, const doub
   uint32_t n = 0;
   for (uint64_t tile = first; tile < tiles; tile += step, ++n) {
     const int slot = (int)(n % PBT_NS);
-    double* buf = ring + (size_t)slot * SLOT;
+    V* buf = ring + (size_t)slot * SLOT_V;
     mbar_wait(&full[unit][slot], (n / PBT_NS) & 1u);
-    double v[1][32];
+    V v[1][32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[0][j] = buf[t + NT * j];   // round-0 layout e = t + NT j
-    Rounds<TP, CB, 0, 1, BarNamed>::run(v, buf, t, bar);
+    Rounds<TP, CB, 0, 1, BarNamed, false, V>::run(v, buf, t, bar);
     bar.sync();                                                  // slot free: refill it
     if (t == 0) {
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -663,9 +673,10 @@ __host__ __device__ constexpr int pas_smem(int L) {
   return (256 >> (L - 5)) * (PAS_NS * 2 * PAS_JS * (1 << (L - 5)) * 16 + padded(1 << L) * 8);
 }
 
-template <int N, int L>
-__global__ void __launch_bounds__(256, 1) k_passAs(const double2* __restrict__ psi, uint64_t a_first, int kcount,
-                                                   double* __restrict__ ws) {
+template <int N, int L, class V = double>
+__global__ void __launch_bounds__(256, 1) k_passAs(const typename Cx<V>::T* __restrict__ psi, uint64_t a_first,
+                                                   int kcount, V* __restrict__ ws) {
+  using C2 = typename Cx<V>::T;
   constexpr int NT = 1 << (L - 5), UNITS = 256 / NT, WPU = NT / 32;   // threads, units, warps per unit
   constexpr int H = N - 1 - L, CB = 13 - H;                            // pass-B tile = 2^13 doubles
   constexpr int SPI = 32 / PAS_JS;                                     // stages per item
@@ -679,8 +690,8 @@ __global__ void __launch_bounds__(256, 1) k_passAs(const double2* __restrict__ p
   const int u = threadIdx.x / NT;
   const uint32_t t = threadIdx.x % NT;
   const int lane = threadIdx.x & 31;
-  double2* ring = reinterpret_cast<double2*>(smem + (size_t)u * UNIT_D);   // [NS][q | r][SD]
-  double* exch = smem + (size_t)u * UNIT_D + PAS_NS * 2 * SD * 2;
+  C2* ring = reinterpret_cast<C2*>(smem + (size_t)u * UNIT_D);   // [NS][q | r][SD]
+  V* exch = reinterpret_cast<V*>(smem + (size_t)u * UNIT_D + PAS_NS * 2 * SD * 2);
   const BarNamed bar{1 + u, NT};
   const uint64_t items = ROWS * (uint64_t)kcount;
   const uint64_t first = (uint64_t)blockIdx.x * UNITS + u, step = (uint64_t)gridDim.x * UNITS;
@@ -700,11 +711,11 @@ __global__ void __launch_bounds__(256, 1) k_passAs(const double2* __restrict__ p
     const int p = 63 - __clzll((long long)a);                   // >= L (a >= 2^L)
     const uint64_t xh = ins0(yh, p - L);
     const uint32_t ahi = (uint32_t)((a & ((1u << L) - 1u)) >> (L - 5));   // r block of block j is j ^ ahi
-    double2* dst = ring + (size_t)slot * 2 * SD;
-    mbar_expect_tx(&full[u][slot], 2 * SD * 16);
-    bulk_g2s(dst, psi + (xh << L) + (size_t)SD * g, SD * 16, &full[u][slot]);
+    C2* dst = ring + (size_t)slot * 2 * SD;
+    mbar_expect_tx(&full[u][slot], 2 * SD * sizeof(C2));
+    bulk_g2s(dst, psi + (xh << L) + (size_t)SD * g, SD * sizeof(C2), &full[u][slot]);
     // blocks {JS g + i} ^ ahi form the aligned group (g ^ (ahi / JS)) permuted by ahi % JS
-    bulk_g2s(dst + SD, psi + ((xh ^ (a >> L)) << L) + (size_t)SD * (g ^ (ahi / PAS_JS)), SD * 16, &full[u][slot]);
+    bulk_g2s(dst + SD, psi + ((xh ^ (a >> L)) << L) + (size_t)SD * (g ^ (ahi / PAS_JS)), SD * sizeof(C2), &full[u][slot]);
   };
   if (t == 0)
     for (int i = 0; i < PAS_NS; ++i)
@@ -716,17 +727,17 @@ __global__ void __launch_bounds__(256, 1) k_passAs(const double2* __restrict__ p
     const int k = (int)(item % (uint64_t)kcount);
     const uint32_t al = (uint32_t)((a_first + (uint64_t)k) & ((1u << L) - 1u));
     const uint32_t alo = al & (NT - 1), ahl = (al >> (L - 5)) % PAS_JS;
-    double v[2][32];
+    V v[2][32];
 #pragma unroll
     for (int gi = 0; gi < SPI; ++gi, ++st) {
       const int slot = (int)(st % PAS_NS);
       mbar_wait(&full[u][slot], (uint32_t)(st / PAS_NS) & 1u);
-      const double2* c = ring + (size_t)slot * 2 * SD;
+      const C2* c = ring + (size_t)slot * 2 * SD;
 #pragma unroll
       for (int i = 0; i < PAS_JS; ++i) {
         const int j = PAS_JS * gi + i;
-        const double2 q = c[NT * i + t];
-        const double2 r = c[SD + NT * (i ^ ahl) + (t ^ alo)];
+        const C2 q = c[NT * i + t];
+        const C2 r = c[SD + NT * (i ^ ahl) + (t ^ alo)];
         v[0][j] = fma(r.x, q.x, r.y * q.y);
         v[1][j] = fma(r.x, q.y, -(r.y * q.x));
       }
@@ -739,9 +750,9 @@ __global__ void __launch_bounds__(256, 1) k_passAs(const double2* __restrict__ p
         if (st + PAS_NS < stages) produce(st + PAS_NS, slot);
       }
     }
-    Rounds<L, 0, 0, 2, BarNamed, true>::run(v, exch, t, bar);
+    Rounds<L, 0, 0, 2, BarNamed, true, V>::run(v, exch, t, bar);
     // position pos = t + NT j (round-0 layout) -> slab-major ((pos >> CB) << (H+CB)) + (y_h << CB) + (pos & (C-1))
-    double* w0 = ws + (size_t)k * 2 * PLANE + (yh << CB);
+    V* w0 = ws + (size_t)k * 2 * PLANE + (yh << CB);
     constexpr uint32_t cm = (1u << CB) - 1u;
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
@@ -1239,6 +1250,9 @@ struct ReduceArgs {
   double scale4[MAXA];  // 4^alpha_i
   const int* err;   // nonzero => a persistent kernel's watchdog fired: results are NaN
 };
+
+#ifdef SRE_API_TU   // non-template kernels: defined once, in sre_api.cu
+
 __global__ void __launch_bounds__(256) k_reduce(const double* __restrict__ partial, ReduceArgs r, double* out) {
   // one block per state; thread i sums slots i, i+256, ... in order, then a fixed binary tree
   // over the 256 thread sums: deterministic for a given nslots
@@ -1279,6 +1293,14 @@ __global__ void __launch_bounds__(256) k_reduce(const double* __restrict__ parti
   }
 }
 
+// FP32 mode: psi (complex128) -> complex64 copy used by the FP32 kernels
+__global__ void k_to_f32(const double2* __restrict__ src, float2* __restrict__ dst, uint64_t n) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const double2 v = __ldg(src + i);
+    dst[i] = make_float2((float)v.x, (float)v.y);
+  }
+}
+
 // sum_x |psi_x|^2 per state (for the norm check), fixed-order block reduce then host/tiny sum
 __global__ void k_norm2_partial(const double2* __restrict__ psi, int N, double* part) {
   const double2* ps = psi + ((size_t)blockIdx.y << N);
@@ -1307,5 +1329,7 @@ __global__ void k_norm2_final(const double* __restrict__ part, int nb, double* o
     out[s] = acc;
   }
 }
+
+#endif  // SRE_API_TU
 
 }  // namespace sre

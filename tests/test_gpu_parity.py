@@ -216,3 +216,22 @@ def test_config5_n24_sampled_and_t_state(sre, oracle_lib):
         w = bin(a).count("1")
         expect = (1.0 ** 2) ** (n - w) * (2 * 0.5 ** 2.0) ** w   # <I>,<Z>: (1, 0); <X>,<Y>: 1/sqrt2 each
         assert abs(g[0] - expect) <= 1e-12 * expect
+
+
+@pytest.mark.parametrize("n", [3, 8, 12, 14, 16, 20, 22])
+def test_fp32_mode_vs_oracle(sre, oracle_lib, n):
+    """Optional FP32 mode (north star): FP32 transform, FP64 accumulation, S_alpha within 1e-4."""
+    psi = si.haar(n, 4000 + n)
+    D = 1 << n
+    lo, hi = (0, D) if n <= 12 else ((D // 2 + 13, D // 2 + 13 + 40) if n < 22 else (D // 2 + 8, D // 2 + 12))
+    al = [1.0, 2.0, 3.0] if n <= 16 else [2.0]
+    t = cuda(psi)
+    g = sre.partial_sums(t, lo, hi, al, precision="fp32").cpu().numpy()[0]
+    o = oracle_lib.sums_fwht(psi, al, a_range=(lo, hi))
+    assert rel(g[:-1], o[:-1]) < 1e-4
+    if 1.0 in al:
+        assert abs(g[-1] - o[-1]) <= 1e-4 * abs(o[-1])
+    if n <= 14:
+        m32, _ = sre.exact(t, [2.0], precision="fp32")
+        m64, _ = sre.exact(t, [2.0])
+        assert abs(m32[0] - m64[0]) < 1e-4 * max(1.0, abs(m64[0]))
