@@ -107,6 +107,18 @@ int sre_partial_sums(const void* psi, int N, int B, uint64_t a_begin, uint64_t a
                      double* sums_dev, void* stream);
 
 /*
+ * sre_x_string_sums -- per-X-string sums for an arbitrary list of X-strings (NEXT-1 building block:
+ * the "energy" of the thermodynamic-integration sampler, Eq. (17) f(X_a) = -ln S(a) with
+ * S(a) = sum_b <psi|X_a Z_b|psi>^4, is one row of this output at alpha = 2; PAPER.md P:376-420,
+ * Alg. 3 line "EvalEnergy").
+ *   a_list : host array [n_a] of X-strings (each < 2^N), any order, repeats allowed.
+ *   out_dev: device [n_a][n_alpha+2], row i = the sums of sre_partial_sums over [a_i, a_i + 1).
+ *   workspace: >= sre_workspace_size(N, 1, n_alpha).  Enqueued on stream (async).
+ */
+int sre_x_string_sums(const void* psi, int N, const uint64_t* a_list, int n_a, const double* alpha, int n_alpha,
+                      void* workspace, size_t ws_bytes, double* out_dev, void* stream);
+
+/*
  * Precision-selecting variants (precision = sre_precision); the plain entry points are SRE_FP64.
  * sre_exact_ex takes B states like sre_exact_batched.  Unknown precision -> SRE_EINVAL (0 bytes
  * from sre_workspace_size_ex).

@@ -20,7 +20,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libsre_b200.so")
 
-__all__ = ["SreError", "load", "exact", "exact_batched", "partial_sums", "finalize", "workspace_size",
+__all__ = ["SreError", "load", "exact", "exact_batched", "partial_sums", "x_string_sums", "finalize", "workspace_size",
            "chi", "norm2", "launch_count", "profile_begin", "profile_end", "LIB_PATH"]
 
 PRECISION = {"fp64": 0, "fp32": 1}   # sre_precision (include/sre.h)
@@ -61,6 +61,7 @@ def load():
             "sre_workspace_size_ex": ([i, i, i, i], ctypes.c_size_t),
             "sre_exact_ex": ([vp, i, i, dp, i, i, dp, dp], i),
             "sre_partial_sums_ex": ([vp, i, i, u64, u64, dp, i, i, vp, ctypes.c_size_t, vp, vp], i),
+            "sre_x_string_sums": ([vp, i, ctypes.POINTER(u64), i, dp, i, vp, ctypes.c_size_t, vp, vp], i),
             "sre_launch_count": ([], u64),
             "sre_profile_begin": ([i], i),
             "sre_profile_end": ([dp, ctypes.POINTER(u64), ctypes.POINTER(u64)], i),
@@ -177,6 +178,31 @@ def partial_sums(psi, a_begin: int, a_end: int, alphas: Sequence[float], out=Non
     _check(lib.sre_partial_sums_ex(ctypes.c_void_p(ptr), n, b, int(a_begin), int(a_end), _dp(al), al.size,
                                    _prec(precision), ctypes.c_void_p(workspace.data_ptr()), workspace.numel(),
                                    ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(st.cuda_stream)))
+    del keep
+    return out
+
+
+def x_string_sums(psi, a_list, alphas: Sequence[float] = (2.0,), out=None, workspace=None, stream=None):
+    """Per-X-string raw sums [len(a_list), n_alpha+2] (row i = sums over the Z-strings of X-string
+    a_list[i]) -- the energy evaluations of the thermodynamic-integration sampler (Alg. 3)."""
+    import torch
+    lib = load()
+    if not (isinstance(psi, torch.Tensor) and psi.is_cuda):
+        raise SreError(1, "x_string_sums needs a cuda complex128 tensor")
+    ptr, n, b, keep = _psi_ptr(psi)
+    if b != 1:
+        raise SreError(1, "x_string_sums takes one state")
+    al = _alphas(alphas)
+    a = np.ascontiguousarray(np.asarray(a_list, dtype=np.uint64).ravel())
+    if out is None:
+        out = torch.empty((a.size, al.size + 2), dtype=torch.float64, device=psi.device)
+    ws_need = workspace_size(n, 1, al.size)
+    if workspace is None or workspace.numel() < ws_need:
+        workspace = torch.empty(ws_need, dtype=torch.uint8, device=psi.device)
+    st = stream if stream is not None else torch.cuda.current_stream(psi.device)
+    _check(lib.sre_x_string_sums(ctypes.c_void_p(ptr), n, a.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                                 a.size, _dp(al), al.size, ctypes.c_void_p(workspace.data_ptr()), workspace.numel(),
+                                 ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(st.cuda_stream)))
     del keep
     return out
 

@@ -536,6 +536,27 @@ int sre_partial_sums_ex(const void* psi, int N, int B, uint64_t a_begin, uint64_
                    precision);
 }
 
+int sre_x_string_sums(const void* psi, int N, const uint64_t* a_list, int n_a, const double* alpha, int n_alpha,
+                      void* workspace, size_t ws_bytes, double* out_dev, void* stream) {
+  g_err[0] = 0;
+  int rc = validate_common(psi, N, 1, alpha, n_alpha);
+  if (rc) return rc;
+  if (!a_list || !workspace || !out_dev) return fail(SRE_EINVAL, "NULL argument");
+  if (n_a < 0) return fail(SRE_EINVAL, "n_a=%d", n_a);
+  for (int i = 0; i < n_a; ++i)
+    if (a_list[i] >= (1ull << N)) return fail(SRE_ERANGE, "a_list[%d]=%llu >= 2^%d", i, (unsigned long long)a_list[i], N);
+  bool dv = false;
+  is_device_ptr(psi, dv);
+  if (!dv) return fail(SRE_EINVAL, "psi must be a device pointer");
+  for (int i = 0; i < n_a; ++i) {
+    rc = run_range(reinterpret_cast<const double2*>(psi), N, 1, a_list[i], a_list[i] + 1, alpha, n_alpha,
+                   reinterpret_cast<char*>(workspace), ws_bytes, out_dev + (size_t)i * (n_alpha + 2),
+                   reinterpret_cast<cudaStream_t>(stream));
+    if (rc) return rc;
+  }
+  return SRE_OK;
+}
+
 int sre_partial_sums(const void* psi, int N, int B, uint64_t a_begin, uint64_t a_end, const double* alpha, int n_alpha,
                      void* workspace, size_t ws_bytes, double* sums_dev, void* stream) {
   g_err[0] = 0;

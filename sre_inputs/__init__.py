@@ -187,3 +187,17 @@ def config3_batch(n: int = 14, b: int = 256, seed: int = 14000):
             states.append(clifford_t(n, 2 * n, seed + i))
             ts.append(None)
     return np.stack(states), ts
+
+
+def mc_streams(seed: int, n_chains: int, n_steps: int, n_qubits: int, move_width: int = 1):
+    """Random numbers drawn by the thermodynamic-integration sampler (Alg. 3), generated
+    up front so the CUDA-path sampler and the oracle's replay consume the identical stream:
+      init    [n_chains]                  initial X-pattern of each beta-chain (uniform in [0, 2^N))
+      flips   [n_steps, n_chains, width]  qubit positions whose a-bit the proposal flips
+      uniform [n_steps, n_chains]         U(0,1) for the Metropolis acceptance test
+    (holds no SRE arithmetic)."""
+    rng = np.random.default_rng(seed)
+    init = rng.integers(0, 1 << n_qubits, size=n_chains, dtype=np.uint64)
+    flips = rng.integers(0, n_qubits, size=(n_steps, n_chains, move_width))
+    uniform = rng.random((n_steps, n_chains))
+    return init, flips, uniform

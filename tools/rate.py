@@ -11,16 +11,17 @@ import sre_inputs as si  # noqa: E402
 
 n, a0, cnt = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3])
 reps = int(sys.argv[4]) if len(sys.argv) > 4 else 2
+prec = sys.argv[5] if len(sys.argv) > 5 else "fp64"
 psi = torch.from_numpy(si.haar(n, 1234)).cuda()
-ws = torch.empty(sre.workspace_size(n, 1, 1), dtype=torch.uint8, device="cuda")
-out = sre.partial_sums(psi, a0, a0 + cnt, [2.0], workspace=ws)
+ws = torch.empty(sre.workspace_size(n, 1, 1, prec), dtype=torch.uint8, device="cuda")
+out = sre.partial_sums(psi, a0, a0 + cnt, [2.0], workspace=ws, precision=prec)
 torch.cuda.synchronize()
 sre.profile_begin(1)
 t0 = time.perf_counter()
 for _ in range(reps):
-    out = sre.partial_sums(psi, a0, a0 + cnt, [2.0], workspace=ws)
+    out = sre.partial_sums(psi, a0, a0 + cnt, [2.0], workspace=ws, precision=prec)
 torch.cuda.synchronize()
 dt = (time.perf_counter() - t0) / reps
 prof = sre.profile_end()
-print(f"N={n} count={cnt}: {dt*1e3:.2f} ms, {cnt * 2.0**n / dt:.3e} Pauli/s, per X-string {dt/cnt*1e6:.2f} us",
+print(f"{prec} N={n} count={cnt}: {dt*1e3:.2f} ms, {cnt * 2.0**n / dt:.3e} Pauli/s, per X-string {dt/cnt*1e6:.2f} us",
       {k: (round(v['ms_sum'] / max(1, v['timed']), 4), v['launched']) for k, v in prof.items() if v['launched']})
