@@ -235,3 +235,13 @@ def test_fp32_mode_vs_oracle(sre, oracle_lib, n):
         m32, _ = sre.exact(t, [2.0], precision="fp32")
         m64, _ = sre.exact(t, [2.0])
         assert abs(m32[0] - m64[0]) < 1e-4 * max(1.0, abs(m64[0]))
+
+
+def test_exact_resumable_matches_exact(sre, tmp_path):
+    from paper_2601_07824_b200.resume import exact_resumable
+    psi = cuda(si.haar(16, 99))
+    j = str(tmp_path / "j.json")
+    assert exact_resumable(psi, [2.0], chunk=4096, journal_path=j, max_chunks=5) is None
+    m, ln = exact_resumable(psi, [2.0], chunk=4096, journal_path=j)
+    m0, ln0 = sre.exact(psi, [2.0])
+    assert abs(m[0] - m0[0]) < 1e-12 and abs(ln - ln0) < 1e-12
