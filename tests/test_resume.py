@@ -30,6 +30,6 @@ def test_journal_key_mismatch(tmp_path):
     import pytest
     from paper_2601_07824_b200.resume import chunked_sums
     j = str(tmp_path / "j.json")
-    chunked_sums(3, [2.0], lambda a0, a1: np.zeros(4), chunk=4, journal_path=j)
+    chunked_sums(3, [2.0], lambda a0, a1: np.zeros(3), chunk=4, journal_path=j)
     with pytest.raises(ValueError):
-        chunked_sums(3, [3.0], lambda a0, a1: np.zeros(4), chunk=4, journal_path=j)
+        chunked_sums(3, [3.0], lambda a0, a1: np.zeros(3), chunk=4, journal_path=j)
