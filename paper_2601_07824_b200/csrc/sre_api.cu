@@ -88,7 +88,7 @@ bool tmem_enabled() {  // opt-in (SRE_TMEM=1): the 4-warp TMEM pass B measured s
 int staged_groups(int N) {
   const char* e = getenv("SRE_KG");
   if (e && atoi(e) > 0) return atoi(e) > 64 ? 64 : atoi(e);
-  return N >= 19 ? 2 : 8;  // N=20: 2 x 8 X-strings x 8 MiB = 128 MiB in flight
+  return 8;  // 64 X-strings per launch pair (N=20: 512 MiB, measured faster than L2-sized 128 MiB: 4.07 vs 4.28 s)
 }
 
 void two_pass_params(int T, int& L, int& H, int& CB) {
