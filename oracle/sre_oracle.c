@@ -272,3 +272,225 @@ int oracle_num_threads(void) {
   return 1;
 #endif
 }
+
+/* =============================================================================================
+ * Qutrit mana (NEXT-3), Sec. 2.1 (Eqs. (4)-(10)) and Sec. 3.3 (Alg. 4, 5,
+ * Eqs. (30)-(36)).  Index x = sum_j x_j 3^j (qutrit j is ternary digit j).
+ * Each function returns sums[2] = { sum_u |<psi|A_u|psi>|, sum_u <psi|A_u|psi> } so that
+ * mana = log2(sums[0] / 3^N) (Eq. (10)) and the Wigner normalisation sum_u W(u) = 1 reads
+ * sums[1] = 3^N.
+ * ============================================================================================= */
+static uint64_t pow3(int n) { uint64_t r = 1; for (int i = 0; i < n; i++) r *= 3; return r; }
+static int digit3(uint64_t x, int j) { for (int i = 0; i < j; i++) x /= 3; return (int)(x % 3); }
+static uint64_t with_digit3(uint64_t x, int j, int d) {
+  uint64_t p = pow3(j);
+  return x - (uint64_t)digit3(x, j) * p + (uint64_t)d * p;
+}
+/* omega^k, omega = e^{2 pi i / 3} */
+static C w3(int k) {
+  k = ((k % 3) + 3) % 3;
+  C c;
+  c.re = cosl(2.0L * 3.14159265358979323846264338327950288L * k / 3.0L);
+  c.im = sinl(2.0L * 3.14159265358979323846264338327950288L * k / 3.0L);
+  return c;
+}
+static C cmul(C a, C b) { C c = {a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re}; return c; }
+
+/* apply X^a (|k> -> |k+a>) or Z^b (|k> -> omega^{b k} |k>) to qutrit j of vector v (in place via tmp) */
+static void q_apply_X(C* v, C* tmp, uint64_t D, int j, int a) {
+  for (uint64_t x = 0; x < D; x++) tmp[with_digit3(x, j, (digit3(x, j) + a) % 3)] = v[x];
+  memcpy(v, tmp, sizeof(C) * D);
+}
+static void q_apply_Z(C* v, uint64_t D, int j, int b) {
+  for (uint64_t x = 0; x < D; x++) v[x] = cmul(w3(b * digit3(x, j)), v[x]);
+}
+
+/* Alg. 4 semantics: <psi| A_ab |psi> with A_ab = D A_0 D^dagger, D = prod_j X_j^{a_j} Z_j^{b_j}
+ * (Eq. (30)) and A_0 |x> = |-x> (Eq. (31)), applied as operators: O(27^N). */
+int oracle_mana_brute(const double* psi, int N, double* sums) {
+  if (N < 1 || N > 6) return 1;
+  const uint64_t D = pow3(N);
+  R s_abs = 0.0L, s_sum = 0.0L;
+  C* v = (C*)malloc(sizeof(C) * D);
+  C* t = (C*)malloc(sizeof(C) * D);
+  for (uint64_t a = 0; a < D; a++)
+    for (uint64_t b = 0; b < D; b++) {
+      for (uint64_t x = 0; x < D; x++) { v[x].re = psi[2 * x]; v[x].im = psi[2 * x + 1]; }
+      /* D^dagger = (prod X^a Z^b)^dagger = prod Z^{-b} X^{-a} : apply X^{-a} first, then Z^{-b} */
+      for (int j = 0; j < N; j++) q_apply_X(v, t, D, j, (3 - digit3(a, j)) % 3);
+      for (int j = 0; j < N; j++) q_apply_Z(v, D, j, (3 - digit3(b, j)) % 3);
+      for (uint64_t x = 0; x < D; x++) {                 /* A_0: |x> -> |-x> */
+        uint64_t y = 0;
+        for (int j = 0; j < N; j++) y += (uint64_t)((3 - digit3(x, j)) % 3) * pow3(j);
+        t[y] = v[x];
+      }
+      memcpy(v, t, sizeof(C) * D);
+      for (int j = 0; j < N; j++) q_apply_Z(v, D, j, digit3(b, j));   /* D = prod X^a Z^b: Z first */
+      for (int j = 0; j < N; j++) q_apply_X(v, t, D, j, digit3(a, j));
+      C e = {0.0L, 0.0L};
+      for (uint64_t y = 0; y < D; y++) {
+        R pr = psi[2 * y], pi = psi[2 * y + 1];
+        e.re += pr * v[y].re + pi * v[y].im;
+        e.im += pr * v[y].im - pi * v[y].re;
+      }
+      s_abs += sqrtl(e.re * e.re + e.im * e.im);
+      s_sum += e.re;
+    }
+  free(v);
+  free(t);
+  sums[0] = (double)s_abs;
+  sums[1] = (double)s_sum;
+  return 0;
+}
+
+/* Phase-space definition, Eqs. (5)-(7): T_ab = omega^{-2^{-1} a b} Z^a X^b (2^{-1} = 2 mod 3),
+ * T_u = (x)_j T_{u_j u'_j}, A_0 = 3^{-N} sum_u T_u, A_u = T_u A_0 T_u^dagger; returns sums of
+ * <psi|A_u|psi> over all 9^N u.  Dense 3^N x 3^N matrices: N <= 3. */
+int oracle_mana_phase_space(const double* psi, int N, double* sums) {
+  if (N < 1 || N > 3) return 1;
+  const uint64_t D = pow3(N), U = D * D;
+  /* single-qutrit T_ab as 3x3 */
+  C T1[9][3][3];
+  for (int a = 0; a < 3; a++)
+    for (int b = 0; b < 3; b++) {
+      C ph = w3(-2 * a * b);
+      for (int r = 0; r < 3; r++)
+        for (int c = 0; c < 3; c++) {
+          /* (Z^a X^b)_{r c} = omega^{a r} [r == c + b] */
+          C val = {0.0L, 0.0L};
+          if (r == (c + b) % 3) val = cmul(ph, w3(a * r));
+          T1[3 * a + b][r][c] = val;
+        }
+    }
+  C* Tu = (C*)malloc(sizeof(C) * D * D);
+  C* A0 = (C*)calloc(D * D, sizeof(C));
+  C* Au = (C*)malloc(sizeof(C) * D * D);
+  C* tmp = (C*)malloc(sizeof(C) * D * D);
+  /* T_u element (r, c) = prod_j T1[u_j][r_j][c_j], u_j in 0..8 (digit pair) */
+  for (uint64_t u = 0; u < U; u++) {
+    for (uint64_t r = 0; r < D; r++)
+      for (uint64_t c = 0; c < D; c++) {
+        C v = {1.0L, 0.0L};
+        uint64_t uu = u;
+        for (int j = 0; j < N; j++) {
+          int uj = (int)(uu % 9);
+          uu /= 9;
+          v = cmul(v, T1[uj][digit3(r, j)][digit3(c, j)]);
+        }
+        Tu[r * D + c] = v;
+      }
+    for (uint64_t k = 0; k < D * D; k++) { A0[k].re += Tu[k].re / (R)D; A0[k].im += Tu[k].im / (R)D; }
+  }
+  R s_abs = 0.0L, s_sum = 0.0L;
+  for (uint64_t u = 0; u < U; u++) {
+    for (uint64_t r = 0; r < D; r++)
+      for (uint64_t c = 0; c < D; c++) {
+        C v = {1.0L, 0.0L};
+        uint64_t uu = u;
+        for (int j = 0; j < N; j++) {
+          int uj = (int)(uu % 9);
+          uu /= 9;
+          v = cmul(v, T1[uj][digit3(r, j)][digit3(c, j)]);
+        }
+        Tu[r * D + c] = v;
+      }
+    /* Au = Tu A0 Tu^dagger */
+    for (uint64_t r = 0; r < D; r++)
+      for (uint64_t c = 0; c < D; c++) {
+        C acc = {0.0L, 0.0L};
+        for (uint64_t k = 0; k < D; k++) { C p = cmul(Tu[r * D + k], A0[k * D + c]); acc.re += p.re; acc.im += p.im; }
+        tmp[r * D + c] = acc;
+      }
+    for (uint64_t r = 0; r < D; r++)
+      for (uint64_t c = 0; c < D; c++) {
+        C acc = {0.0L, 0.0L};
+        for (uint64_t k = 0; k < D; k++) {
+          C td = {Tu[c * D + k].re, -Tu[c * D + k].im};     /* (Tu^dagger)_{k c} = conj(Tu_{c k}) */
+          C p = cmul(tmp[r * D + k], td);
+          acc.re += p.re;
+          acc.im += p.im;
+        }
+        Au[r * D + c] = acc;
+      }
+    C e = {0.0L, 0.0L};                                     /* <psi|Au|psi> */
+    for (uint64_t r = 0; r < D; r++)
+      for (uint64_t c = 0; c < D; c++) {
+        C pc = {psi[2 * c], psi[2 * c + 1]};
+        C pr = {psi[2 * r], -psi[2 * r + 1]};
+        C p = cmul(pr, cmul(Au[r * D + c], pc));
+        e.re += p.re;
+        e.im += p.im;
+      }
+    s_abs += sqrtl(e.re * e.re + e.im * e.im);
+    s_sum += e.re;
+  }
+  free(Tu);
+  free(A0);
+  free(Au);
+  free(tmp);
+  sums[0] = (double)s_abs;
+  sums[1] = (double)s_sum;
+  return 0;
+}
+
+/* Alg. 5: for each a, alpha = X_a psi (alpha_x = psi_{x-a}), v_x = conj(alpha_x) alpha_{-x}
+ * (Eq. (32)), chi = F_3^{(x)N} v with (F_3)_{jk} = omega^{2jk} (Eq. (35)), m += sum_b |chi_b|.
+ * Naive radix-3 pass per digit.  a in [a_lo, a_hi); OpenMP over a. */
+int oracle_mana_fwht(const double* psi, int N, uint64_t a_lo, uint64_t a_hi, double* sums) {
+  if (N < 1 || N > 16 || a_lo > a_hi) return 1;
+  const uint64_t D = pow3(N);
+  if (a_hi > D) return 1;
+  const uint64_t na = a_hi - a_lo;
+  R* pa = (R*)calloc((size_t)(na ? na : 1) * 2, sizeof(R));
+  uint64_t* p3 = (uint64_t*)malloc(sizeof(uint64_t) * (N + 1));
+  for (int j = 0; j <= N; j++) p3[j] = pow3(j);
+#pragma omp parallel
+  {
+    C* v = (C*)malloc(sizeof(C) * D);
+    int* dg = (int*)malloc(sizeof(int) * N);
+#pragma omp for schedule(dynamic, 1)
+    for (int64_t k = 0; k < (int64_t)na; k++) {
+      const uint64_t a = a_lo + (uint64_t)k;
+      int ad[32];
+      for (int j = 0; j < N; j++) ad[j] = (int)((a / p3[j]) % 3);
+      for (uint64_t x = 0; x < D; x++) {
+        uint64_t i1 = 0, i2 = 0;
+        for (int j = 0; j < N; j++) {
+          dg[j] = (int)((x / p3[j]) % 3);
+          i1 += (uint64_t)((dg[j] - ad[j] + 3) % 3) * p3[j];         /* x - a      */
+          i2 += (uint64_t)((6 - dg[j] - ad[j]) % 3) * p3[j];         /* (-x) - a   */
+        }
+        C al = {psi[2 * i1], psi[2 * i1 + 1]}, am = {psi[2 * i2], psi[2 * i2 + 1]};
+        v[x].re = al.re * am.re + al.im * am.im;                     /* conj(alpha_x) alpha_{-x} */
+        v[x].im = al.re * am.im - al.im * am.re;
+      }
+      C w[3] = {w3(0), w3(1), w3(2)};                                 /* omega^k, k mod 3 */
+      for (int j = 0; j < N; j++) {                                   /* F_3 on digit j */
+        const uint64_t h = p3[j];
+        for (uint64_t base = 0; base < D; base += 3 * h)
+          for (uint64_t o = 0; o < h; o++) {
+            C u[3], y[3];
+            for (int r = 0; r < 3; r++) u[r] = v[base + o + (uint64_t)r * h];
+            for (int r = 0; r < 3; r++) {
+              y[r].re = 0.0L; y[r].im = 0.0L;
+              for (int c = 0; c < 3; c++) { C p = cmul(w[(2 * r * c) % 3], u[c]); y[r].re += p.re; y[r].im += p.im; }
+            }
+            for (int r = 0; r < 3; r++) v[base + o + (uint64_t)r * h] = y[r];
+          }
+      }
+      R sa = 0.0L, ss = 0.0L;
+      for (uint64_t b = 0; b < D; b++) { sa += sqrtl(v[b].re * v[b].re + v[b].im * v[b].im); ss += v[b].re; }
+      pa[2 * k] = sa;
+      pa[2 * k + 1] = ss;
+    }
+    free(v);
+    free(dg);
+  }
+  R t0 = 0.0L, t1 = 0.0L;
+  for (uint64_t k = 0; k < na; k++) { t0 += pa[2 * k]; t1 += pa[2 * k + 1]; }
+  sums[0] = (double)t0;
+  sums[1] = (double)t1;
+  free(pa);
+  free(p3);
+  return 0;
+}
