@@ -167,6 +167,43 @@ uint64_t sre_launch_count(void);
 int sre_profile_begin(int stride);
 int sre_profile_end(double* ms_sum, uint64_t* n_timed, uint64_t* n_launched);
 
+/* ============================================================================================
+ * Pure-state qutrit mana (NEXT-3): Algorithm 5, Sec. 3.3.2.
+ *
+ * psi: 3^N complex128 amplitudes (interleaved re, im; 16-byte aligned), index x = sum_j x_j 3^j
+ * (qutrit j = ternary digit j; DESIGN C19).  For each X-string a in Z_3^N the library forms
+ * v_x = conj(psi_{x-a}) psi_{-x-a} (Eq. (32), digit-wise mod 3), chi(a) = F_3^{(x)N} v with
+ * (F_3)_{jk} = omega^{2jk}, omega = e^{2 pi i/3} (Eqs. (35)-(36)), and accumulates in FP64
+ *   S_abs = sum_{a,b} |chi_b(a)|      S_sum = sum_{a,b} chi_b(a)  ( = 3^N ||psi||^2 ).
+ * Mana = log2(S_abs / 3^N) (Eq. (10) / (11), DESIGN C18).  N in [1, SRE_MANA_MAX_N].
+ * ============================================================================================ */
+#define SRE_MANA_MAX_N 16
+
+/* Bytes of device workspace sre_mana_partial_sums needs for N (0 if N is out of range).  Less
+ * is accepted down to the size of one X-string pair; fewer pairs then run per launch. */
+size_t sre_mana_workspace_size(int N);
+
+/*
+ * sre_mana_partial_sums -- asynchronous building block (multi-GPU shards, checkpointed ranges).
+ *   psi       : DEVICE pointer to 3^N complex128 (not modified; not checked for normalisation).
+ *   [a_begin, a_end) : X-string range, 0 <= a_begin <= a_end <= 3^N (X-string a as a base-3 integer).
+ *   workspace : device buffer, 256-byte aligned, ws_bytes bytes (>= one pair; see above).
+ *   sums_dev  : device double[2] <- (S_abs, S_sum) restricted to the range (overwritten).
+ *   stream    : cudaStream_t (NULL = legacy default stream).  Enqueues only; no host sync.
+ * Errors: SRE_EINVAL (NULL / misaligned / host psi), SRE_ERANGE (N or range), SRE_EWORKSPACE,
+ * SRE_ECUDA.  Deterministic: bitwise identical results for the same inputs on the same device.
+ */
+int sre_mana_partial_sums(const void* psi, int N, uint64_t a_begin, uint64_t a_end, void* workspace,
+                          size_t ws_bytes, double* sums_dev, void* stream);
+
+/*
+ * sre_mana -- synchronous convenience: mana of one state, psi a HOST or DEVICE pointer.
+ *   out_mana  : log2(S_abs / 3^N).   out_norm2 (may be NULL): S_sum / 3^N = ||psi||^2.
+ * Returns SRE_ENOTNORM (with out_norm2 set, out_mana untouched) when | ||psi||^2 - 1 | > 1e-8.
+ * Uses library-owned cached device buffers (one per process, guarded by a mutex).
+ */
+int sre_mana(const void* psi, int N, double* out_mana, double* out_norm2);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,95 @@
+"""Pure-state qutrit mana (NEXT-3) -- thin ctypes binding over the C ABI (include/sre.h,
+``sre_mana*``).  Argument marshalling only: every step runs in libsre_b200.so (csrc/mana.cu).
+
+    m, norm2 = mana(psi)                       # P:869-884 Alg. 5; log2(sum |chi| / 3^N), Eq. (10)
+    sums = partial_sums(psi, a0, a1)           # device [2] = (sum |chi|, sum chi) over X-strings [a0, a1)
+
+psi: complex128 of length 3^N (qutrit j = ternary digit j of the index), numpy or torch.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import SreError, _check, load
+
+_ready = False
+
+
+def _lib():
+    global _ready
+    lib = load()
+    if not _ready:
+        vp, dp, i, u64 = ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.c_int, ctypes.c_uint64
+        lib.sre_mana_workspace_size.argtypes = [i]
+        lib.sre_mana_workspace_size.restype = ctypes.c_size_t
+        lib.sre_mana_partial_sums.argtypes = [vp, i, u64, u64, vp, ctypes.c_size_t, vp, vp]
+        lib.sre_mana_partial_sums.restype = i
+        lib.sre_mana.argtypes = [vp, i, dp, dp]
+        lib.sre_mana.restype = i
+        _ready = True
+    return lib
+
+
+def n_qutrits(dim: int) -> int:
+    n, d = 0, 1
+    while d < dim:
+        d *= 3
+        n += 1
+    if d != dim or dim < 3:
+        raise SreError(2, f"state length {dim} is not 3^N with N >= 1")
+    return n
+
+
+def _ptr(psi):
+    try:
+        import torch
+        if isinstance(psi, torch.Tensor):
+            if psi.dtype != torch.complex128 or psi.dim() != 1:
+                raise SreError(1, "psi must be a 1-D complex128 tensor")
+            t = psi.contiguous()
+            return t.data_ptr(), n_qutrits(t.numel()), t
+    except ImportError:
+        pass
+    a = np.ascontiguousarray(np.asarray(psi))
+    if a.dtype != np.complex128 or a.ndim != 1:
+        raise SreError(1, "psi must be a 1-D complex128 array")
+    return a.ctypes.data, n_qutrits(a.size), a
+
+
+def workspace_size(n: int) -> int:
+    return int(_lib().sre_mana_workspace_size(n))
+
+
+def mana(psi):
+    """(mana, ||psi||^2) of a host or cuda state via sre_mana (synchronous)."""
+    lib = _lib()
+    ptr, n, keep = _ptr(psi)
+    m = ctypes.c_double(0.0)
+    n2 = ctypes.c_double(0.0)
+    _check(lib.sre_mana(ctypes.c_void_p(ptr), n, ctypes.byref(m), ctypes.byref(n2)))
+    del keep
+    return m.value, n2.value
+
+
+def partial_sums(psi, a_begin: int, a_end: int, out=None, workspace=None, stream=None):
+    """Device float64[2] = (sum |chi_b(a)|, sum chi_b(a)) over X-strings a in [a_begin, a_end),
+    enqueued on ``stream`` (default: torch's current stream).  psi must be a cuda tensor."""
+    import torch
+    lib = _lib()
+    if not (isinstance(psi, torch.Tensor) and psi.is_cuda):
+        raise SreError(1, "partial_sums needs a cuda complex128 tensor")
+    ptr, n, keep = _ptr(psi)
+    dev = psi.device
+    if out is None:
+        out = torch.empty(2, dtype=torch.float64, device=dev)
+    need = workspace_size(n)
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=dev)
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    _check(lib.sre_mana_partial_sums(ctypes.c_void_p(ptr), n, int(a_begin), int(a_end),
+                                     ctypes.c_void_p(workspace.data_ptr()), workspace.numel(),
+                                     ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(st.cuda_stream)))
+    del keep
+    return out
