@@ -37,6 +37,12 @@ CONFIGS = {
     "c3": ("256 x N=14 Clifford+T states, alpha=2 (BASELINE config 3)", 14, 256, [2.0], 14000),
     "c5": ("N=24 seeded Haar state, alpha=2 (BASELINE config 5)", 24, 1, [2.0], 24001),
 }
+# Pure-state qutrit mana (NEXT-3, Alg. 5): name -> (workload label, N qutrits, brick-wall depth, seed)
+MANA_CONFIGS = {
+    "m12": ("N=12 qutrit brick-wall state, depth 4 (pure-state mana, PAPER Table II row N=12, P:1449-1466)", 12, 4, 12012),
+    "m14": ("N=14 qutrit brick-wall state, depth 4 (pure-state mana, PAPER Table II row N=14, P:1449-1466)", 14, 4, 14014),
+}
+MANA_METRIC = "exact pure-state qutrit mana, phase-space points/s (9^N per state)"
 FP64_OPS_PER_CLK_SM = 64        # B200 FP64 pipe (measured 63.9/clk/SM, profiles/r01_microbench.json)
 
 
@@ -158,16 +164,192 @@ def run_reference(args):
     return 0
 
 
+def mana_state(cfg):
+    import sre_inputs.qutrit as q
+    _, n, depth, seed = MANA_CONFIGS[cfg]
+    return q.brickwall(n, depth, seed)
+
+
+def mana_cpu_sample(psi, n, label, seconds_target):
+    """Oracle (Alg. 5, long double, OpenMP) over a bounded slice [0, k) of the X-strings."""
+    import oracle
+    from oracle import mana as om
+    threads = oracle.num_threads()
+    k = max(threads, 1)
+    t0 = time.perf_counter()
+    om.sums_fwht(psi, (0, k))
+    per_a = (time.perf_counter() - t0) / k
+    k2 = int(min(3 ** n, max(threads, seconds_target / max(per_a, 1e-9))))
+    k2 = max(threads, (k2 // threads) * threads)
+    t0 = time.perf_counter()
+    om.sums_fwht(psi, (0, k2))
+    dt = time.perf_counter() - t0
+    return {"value": k2 * float(3 ** n) / dt, "unit": "phase-space points/s", "cores": threads, "kind": "oracle",
+            "sample": f"oracle mana fwht (Alg. 5, long double) over X-strings [0, {k2}) of the {label}; "
+                      f"{k2} x 3^{n} points in {dt:.2f} s", "seconds": dt}, k2
+
+
+def run_mana_reference(args):
+    if int(os.environ.get("RANK", "0")) != 0:
+        return 0
+    label, n, depth, seed = MANA_CONFIGS[args.config]
+    import oracle
+    oracle.build()
+    psi = mana_state(args.config)
+    budget = 150.0 / max(1, args.steps + args.warmup)
+    cb, k = mana_cpu_sample(psi, n, label, budget)
+    from oracle import mana as om
+    for _ in range(args.warmup):
+        om.sums_fwht(psi, (0, k))
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        om.sums_fwht(psi, (0, k))
+        times.append(time.perf_counter() - t0)
+    dt = sum(times)
+    value = args.steps * k * float(3 ** n) / dt
+    cb.update({"value": value, "sample": f"oracle mana fwht over X-strings [0, {k}) per step ({k} of 3^{n})"})
+    print(json.dumps({
+        "impl": "reference", "metric": MANA_METRIC, "value": value, "unit": "phase-space points/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64 (long double accum)",
+        "data": "synthetic", "config": {"workload": label, "N": n, "depth": depth, "seed": seed,
+                                        "x_strings_per_step": k},
+        "cpu_baseline": cb,
+        "e2e": {"value": value, "unit": "phase-space points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+    return 0
+
+
+def main_mana(args):
+    """A step = the full Alg. 5 sweep of one N-qutrit state (all 3^N X-strings, 9^N phase-space
+    points), sharded over ranks by contiguous X-string ranges, one all_reduce of 2 doubles, and the
+    host log2 of Eq. (10)."""
+    import math
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2601_07824_b200 as sre
+    from paper_2601_07824_b200 import qutrit
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    label, n, depth, seed = MANA_CONFIGS[args.config]
+    na = 3 ** n
+    lo, hi = na * rank // world, na * (rank + 1) // world
+    psi_host = mana_state(args.config)
+    psi = torch.from_numpy(psi_host).to(dev)
+    ws = torch.empty(qutrit.workspace_size(n), dtype=torch.uint8, device=dev)
+    sums = torch.empty(2, dtype=torch.float64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        qutrit.partial_sums(psi, lo, hi, out=sums, workspace=ws, stream=stream)
+        if world > 1:
+            dist.all_reduce(sums)
+        h = sums.cpu().numpy()
+        return math.log2(h[0] / na), h[1] / na
+
+    for _ in range(max(args.warmup, 0)):
+        m, n2 = step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    launches0 = sre.launch_count()
+    sre.profile_begin(max(1, args.profile_stride // 4))
+    step_ms = []
+    for _ in range(args.steps):
+        flush.fill_(1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        m, n2 = step()
+        e1.record(stream)
+        e1.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+    prof = sre.profile_end()
+    launches = sre.launch_count() - launches0
+    clk = clocks.stop()
+    tot_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+        dist.barrier()
+    pts = 9.0 ** n
+    value = args.steps * pts / (tot_ms * 1e-3)
+    e2e = None
+    if world == 1:
+        pinned = torch.from_numpy(psi_host).pin_memory()
+        t_e = []
+        for _ in range(max(1, min(args.steps, 2))):
+            t0 = time.perf_counter()
+            qutrit.mana(pinned)                               # H2D + sweep + D2H of the 2 sums
+            t_e.append(time.perf_counter() - t0)
+        e2e = {"value": pts * len(t_e) / sum(t_e), "unit": "phase-space points/s",
+               "h2d_bytes_per_step": int(psi_host.nbytes), "d2h_bytes_per_step": 16,
+               "ms_per_step": 1e3 * sum(t_e) / len(t_e)}
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+    peaks, _ = load_peaks()
+    kinds = {k: v for k, v in prof.items() if v["timed"] > 0 and k != "aux"}
+    share = {k: v["ms_sum"] / v["timed"] * v["launched"] for k, v in kinds.items()}
+    dom = max(share, key=share.get)
+    avg_ms = prof[dom]["ms_sum"] / prof[dom]["timed"]
+    pts_per_launch = pts * args.steps / max(1, world) / prof[dom]["launched"]
+    # FP64 ops per phase-space point (DESIGN.md section 15): pass A = gen 5 + 2 L, pass B = 2 H + 2
+    L = {9: 5, 10: 6, 11: 6, 12: 7, 13: 7, 14: 7, 15: 8, 16: 8}.get(n, n)
+    ops_pt = {"pass_a": 5 + 2 * L, "pass_b": 2 * (n - L) + 2, "single_pass": 5 + 2 * n + 2}[dom]
+    sm_mhz = (clk or {}).get("sm_max_mhz", peaks.get("sm_max_mhz", 1965.0))
+    peak = FP64_OPS_PER_CLK_SM * 148 * sm_mhz * 1e6 / 1e12
+    achieved = ops_pt * pts_per_launch / (avg_ms * 1e-3) / 1e12
+    roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s (FP64 ops)", "frac": achieved / peak,
+            "traffic": None, "kernel": dom, "avg_launch_ms": avg_ms, "launches_timed": prof[dom]["timed"],
+            "share_of_step": share[dom] / tot_ms if world == 1 else None, "ops_per_point": ops_pt,
+            "peak_source": f"64 FP64 ops/clk/SM x 148 SMs x {sm_mhz:.0f} MHz",
+            "note": "measured limiter is the L1TEX/shared-memory data pipe (profiles/r01_ncu_summary_mana14.txt)"}
+    line = {
+        "metric": MANA_METRIC, "value": value, "unit": "phase-space points/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": label, "N": n, "depth": depth, "seed": seed, "x_string_shards": world,
+                   "l2": "flushed between steps (256 MiB write)",
+                   "step": "mana partial sums over all 3^N X-strings + allreduce + log2"},
+        "roofline": roof, "gpu_launches": int(launches), "clocks": clk, "e2e": e2e,
+        "result": {"mana": m, "norm2": n2}, "profile": prof,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        import oracle
+        oracle.build()
+        line["cpu_baseline"], _ = mana_cpu_sample(psi_host, n, label, 15.0)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS) + sorted(MANA_CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-stride", type=int, default=16)
     args = ap.parse_args()
+    if args.config in MANA_CONFIGS:
+        return run_mana_reference(args) if args.impl == "reference" else main_mana(args)
     if args.impl == "reference":
         return run_reference(args)
 

@@ -22,6 +22,8 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -145,6 +147,44 @@ __device__ __forceinline__ void stages(double2* tile, double& aa, double& as) {
   }
 }
 
+// Functor-driven stage: same fibers as stage(), element e read through ld(e) and written through
+// st(e, v) -- lets the first stage read global memory and the last write it (or accumulate).
+template <int M, int S, int J, int g, class Ld, class St>
+__device__ __forceinline__ void stage_f(Ld ld, St st) {
+  constexpr int R = p3(g);
+  constexpr int sj = p3(J);
+  constexpr int fibers = p3(M - g) * S;
+  for (int f = threadIdx.x; f < fibers; f += kThreads) {
+    const int c = f % S, rest = f / S;
+    const int lo = rest % sj, hi = rest / sj;
+    const int base = (hi * sj * R + lo) * S + c;
+    double2 r[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) r[k] = ld(base + k * sj * S);
+    reg_f3<g>(r);
+#pragma unroll
+    for (int k = 0; k < R; ++k) st(base + k * sj * S, r[k]);
+  }
+}
+
+// Digits [J, M) of a 3^M x S tile; the first stage (if FIRST) loads through ldf, the last stores
+// through stl, intermediate stages go through shared memory.
+template <int M, int S, int J, bool FIRST, class LdF, class StL>
+__device__ __forceinline__ void stages_f(double2* tile, LdF ldf, StL stl) {
+  if constexpr (J < M) {
+    constexpr int g = (M - J >= 2) ? 2 : 1;
+    constexpr bool last = (J + g == M);
+    auto lds = [&](int e) { return tile[e]; };
+    auto sts = [&](int e, double2 v) { tile[e] = v; };
+    if constexpr (FIRST && last) stage_f<M, S, J, g>(ldf, stl);
+    else if constexpr (FIRST) stage_f<M, S, J, g>(ldf, sts);
+    else if constexpr (last) stage_f<M, S, J, g>(lds, stl);
+    else stage_f<M, S, J, g>(lds, sts);
+    if constexpr (!last) __syncthreads();
+    stages_f<M, S, J + g, false>(tile, ldf, stl);
+  }
+}
+
 // Fixed-order block reduction of (aa, as); thread 0 adds the result to slots[2*blockIdx.x..].
 __device__ __forceinline__ void flush(double aa, double as, double* slots) {
   __shared__ double red[2][kThreads / 32];
@@ -181,11 +221,11 @@ struct RowArgs {
 };
 
 // Pass A / single pass.  Row h of pair p: w_l = v1_{h,l} + i v2_{h,l}, F_3 over the L low digits.
-template <int L, bool FINAL>
-__global__ void __launch_bounds__(kThreads) k_mana_row(RowArgs A) {
-  constexpr int G = (L > 5) ? L - 5 : 0;     // digits done in registers
+template <int L, bool FINAL, int G = (L > 5 ? L - 5 : 0)>
+__global__ void __launch_bounds__(kThreads, 2) k_mana_row(RowArgs A) {
+  // G: low digits done in registers (3^G consecutive l per thread group)
   constexpr int RG = p3(G);
-  constexpr int NT = p3(L - G);              // thread groups per row (<= 243)
+  constexpr int NT = p3(L - G);              // thread groups per row
   constexpr int NL = p3(L);
   extern __shared__ double2 tile[];
   const int nh = p3(A.H);
@@ -195,8 +235,7 @@ __global__ void __launch_bounds__(kThreads) k_mana_row(RowArgs A) {
     const int pl = (int)(it / nh), h = (int)(it % nh);
     const uint64_t a1 = A.a_begin + 2 * (A.pair0 + pl);
     const bool two = a1 + 1 < A.a_end;
-    const int t = threadIdx.x;
-    if (t < NT) {
+    for (int t = threadIdx.x; t < NT; t += kThreads) {
       double2 r[RG];
       // X-string a1 (and a2 = a1 + 1): rows of psi and the shifted low-index bases
       int rs[2], rn[2], ls[2], ln[2], alo[2];
@@ -286,6 +325,145 @@ __global__ void __launch_bounds__(kThreads) k_mana_col(ColArgs A) {
   flush(aa, as, A.slots);
 }
 
+// ---------------------------------------------------------------------------------------------
+// Staged two-pass (N = 9..14): rows of psi staged in shared memory and shared by the PP pairs of
+// one item; the workspace is column-blocked, ws[pair][cb][h][c] (S columns per block), so that a
+// pass-B tile is one contiguous 3^H x S chunk.
+// ---------------------------------------------------------------------------------------------
+struct RowSArgs {
+  const double2* psi;
+  double2* ws;
+  uint64_t a_begin, a_end;
+  uint64_t pair0;       // first pair of this launch
+  int npairs;           // pairs in this launch
+  int H;                // high digits
+  int S;                // columns per workspace block
+  int PP;               // pairs per item
+};
+
+template <int L, int G>
+__global__ void __launch_bounds__(kThreads) k_mana_rowS(RowSArgs A) {
+  constexpr int RG = p3(G);
+  constexpr int NT = p3(L - G);
+  constexpr int NL = p3(L);
+  extern __shared__ double2 smem[];
+  double2* rowA = smem;            // psi row (h - a_hi)
+  double2* rowB = smem + NL;       // psi row (-h - a_hi)
+  double2* tile = smem + 2 * NL;
+  const int nh = p3(A.H);
+  const int nchunk = (A.npairs + A.PP - 1) / A.PP;
+  const int nblk = (NL + A.S - 1) / A.S;
+  const long items = (long)nh * nchunk;
+  for (long it = blockIdx.x; it < items; it += gridDim.x) {
+    const int h = (int)(it / nchunk), ch = (int)(it % nchunk);
+    const int p_lo = ch * A.PP, p_hi = min(A.npairs, p_lo + A.PP);
+    int cur = -1;
+    for (int pl = p_lo; pl < p_hi; ++pl) {
+      const uint64_t a1 = A.a_begin + 2 * (A.pair0 + pl);
+      const bool two = a1 + 1 < A.a_end;
+      const int ah1 = (int)(a1 / NL);
+      if (ah1 != cur) {                       // (re)stage the two rows this a_hi needs
+        __syncthreads();
+        int hs, hn;
+        tshift_rt(h, ah1, A.H, hs, hn);
+        const double2* r1 = A.psi + (size_t)hs * NL;
+        const double2* r2 = A.psi + (size_t)hn * NL;
+        for (int l = threadIdx.x; l < NL; l += kThreads) {
+          rowA[l] = __ldg(r1 + l);
+          rowB[l] = __ldg(r2 + l);
+        }
+        __syncthreads();
+        cur = ah1;
+      }
+      const int al1 = (int)(a1 % NL);
+      const uint64_t a2 = a1 + 1;
+      const int ah2 = (int)(a2 / NL), al2 = (int)(a2 % NL);
+      const bool staged2 = (ah2 == ah1);
+      int g2s = 0, g2n = 0;                   // rows for a2 when it crosses an a_hi boundary
+      if (two && !staged2) tshift_rt(h, ah2, A.H, g2s, g2n);
+      for (int t = threadIdx.x; t < NT; t += kThreads) {
+        double2 r[RG];
+        int us1, un1, us2, un2;
+        tshift<L - G>(t, al1 / RG, us1, un1);
+        tshift<L - G>(t, al2 / RG, us2, un2);
+#pragma unroll
+        for (int i = 0; i < RG; ++i) {
+          int ss, sn;
+          tshift<G>(i, al1 % RG, ss, sn);
+          double2 x1 = rowA[us1 * RG + ss];
+          double2 x2 = rowB[un1 * RG + sn];
+          double2 w;
+          w.x = x1.x * x2.x + x1.y * x2.y;
+          w.y = x1.x * x2.y - x1.y * x2.x;
+          if (two) {
+            tshift<G>(i, al2 % RG, ss, sn);
+            if (staged2) {
+              x1 = rowA[us2 * RG + ss];
+              x2 = rowB[un2 * RG + sn];
+            } else {
+              x1 = __ldg(A.psi + (size_t)g2s * NL + us2 * RG + ss);
+              x2 = __ldg(A.psi + (size_t)g2n * NL + un2 * RG + sn);
+            }
+            w.x -= x1.x * x2.y - x1.y * x2.x;   // + i v2
+            w.y += x1.x * x2.x + x1.y * x2.y;
+          }
+          r[i] = w;
+        }
+        reg_f3<G>(r);
+#pragma unroll
+        for (int i = 0; i < RG; ++i) tile[t * RG + i] = r[i];
+      }
+      __syncthreads();
+      double2* dst = A.ws + (size_t)pl * ((size_t)nblk * nh * A.S) + (size_t)h * A.S;
+      const int S = A.S, bs = nh * A.S;
+      auto to_ws = [&](int l, double2 v) {     // last stage: straight to the column-blocked workspace
+        const int cb = l / S;
+        __stcg(dst + (size_t)cb * bs + (l - cb * S), v);
+      };
+      auto no_ld = [&](int e) { return tile[e]; };
+      stages_f<L, 1, G, false>(tile, no_ld, to_ws);
+      __syncthreads();
+    }
+  }
+}
+
+struct ColCArgs {
+  const double2* ws;    // [pairs][nblk][3^H][S]
+  double* slots;
+  int npairs;
+  int L;
+};
+
+// Pass B on the column-blocked workspace: one contiguous 3^H x S tile per item.
+template <int H, int S>
+__global__ void __launch_bounds__(kThreads) k_mana_colC(ColCArgs A) {
+  extern __shared__ double2 tile[];
+  constexpr int NH = p3(H);
+  constexpr int E = NH * S;
+  const int NL = p3(A.L);
+  const int nblk = (NL + S - 1) / S;
+  const long items = (long)A.npairs * nblk;
+  double aa = 0.0, as = 0.0;
+  for (long it = blockIdx.x; it < items; it += gridDim.x) {
+    const int cb = (int)(it % nblk);
+    const int ncol = min(S, NL - cb * S);
+    const double2* src = A.ws + (size_t)it * E;
+    auto acc = [&](int, double2 v) {
+      aa += fabs(v.x) + fabs(v.y);
+      as += v.x + v.y;
+    };
+    if (ncol == S) {                          // first stage straight from the contiguous tile
+      auto ld = [&](int e) { return __ldcs(src + e); };
+      stages_f<H, S, 0, true>(tile, ld, acc);
+    } else {
+      auto ld = [&](int e) { return (e % S) < ncol ? __ldcs(src + e) : make_double2(0.0, 0.0); };
+      stages_f<H, S, 0, true>(tile, ld, acc);
+    }
+    __syncthreads();
+  }
+  flush(aa, as, A.slots);
+}
+
 // Fixed-order sum of the per-CTA slots: out = (S_abs, S_sum).
 __global__ void __launch_bounds__(256) k_mana_reduce(const double* slots, int n, double* out) {
   __shared__ double sa[256], ss[256];
@@ -331,6 +509,8 @@ using mana::kSlots;
 struct MPlan {
   int N = 0, L = 0, H = 0, S = 0;
   bool single = false;
+  bool staged = false;    // N = 9..14: k_mana_rowS + k_mana_colC
+  int PP = 1;             // pairs per pass-A item (staged)
   size_t row_smem = 0, col_smem = 0;
   size_t row_bytes = 0;   // workspace bytes per pair (3^N complex)
   uint64_t P = 0;         // preferred pairs per launch
@@ -340,8 +520,8 @@ constexpr size_t kSlotBytes = (size_t)kSlots * 2 * sizeof(double);
 
 void make_mplan(int N, MPlan& m) {
   static const int tab[17][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}, {0, 0, 0},
-                                 {0, 0, 0}, {0, 0, 0}, {5, 4, 32}, {6, 4, 32}, {6, 5, 16}, {7, 5, 16},
-                                 {7, 6, 8}, {8, 6, 8}, {8, 7, 4}, {8, 8, 2}};
+                                 {0, 0, 0}, {0, 0, 0}, {5, 4, 32}, {6, 4, 32}, {6, 5, 16}, {7, 5, 8},
+                                 {7, 6, 4}, {7, 7, 2}, {8, 7, 4}, {8, 8, 2}};
   m.N = N;
   if (N <= 8) {
     m.single = true;
@@ -352,14 +532,29 @@ void make_mplan(int N, MPlan& m) {
     m.H = tab[N][1];
     m.S = tab[N][2];
   }
-  m.row_smem = (size_t)p3(m.L) * sizeof(double2);
+  if (!m.single) {  // SRE_MANA_PLAN="L,H,S" overrides the split (experiments; must match N)
+    const char* e = std::getenv("SRE_MANA_PLAN");
+    int l = 0, h = 0, c = 0;
+    if (e && std::sscanf(e, "%d,%d,%d", &l, &h, &c) == 3 && l + h == N) {
+      m.L = l;
+      m.H = h;
+      m.S = c;
+    }
+  }
+  m.staged = !m.single && m.L <= 7 && std::getenv("SRE_MANA_UNSTAGED") == nullptr;
+  m.row_smem = (size_t)p3(m.L) * sizeof(double2) * (m.staged ? 3 : 1);
   m.col_smem = m.single ? 0 : (size_t)p3(m.H) * m.S * sizeof(double2);
   m.row_bytes = (size_t)p3(N) * sizeof(double2);
+  if (m.staged)  // column-blocked: the last block of columns is padded to S
+    m.row_bytes = (size_t)((p3(m.L) + m.S - 1) / m.S) * m.S * p3(m.H) * sizeof(double2);
   if (m.single) {
     m.P = 0;
   } else {
-    uint64_t P = (64ull << 20) / m.row_bytes;
+    // L2-resident workspace (64 MiB) while a pair's transform is small; from 16 MiB per pair on
+    // the workspace streams through HBM anyway, so 8 pairs share each staged psi row.
+    uint64_t P = m.row_bytes >= (16ull << 20) ? 8 : (64ull << 20) / m.row_bytes;
     m.P = P < 1 ? 1 : (P > 4096 ? 4096 : P);
+    m.PP = m.staged ? 8 : 1;
   }
 }
 
@@ -367,6 +562,28 @@ size_t ws_needed(const MPlan& m, uint64_t P) { return kSlotBytes + (m.single ? 0
 
 using RowFn = void (*)(mana::RowArgs);
 using ColFn = void (*)(mana::ColArgs);
+using RowSFn = void (*)(mana::RowSArgs);
+using ColCFn = void (*)(mana::ColCArgs);
+
+RowSFn rows_fn(int L) {
+  switch (L) {
+    case 5: return mana::k_mana_rowS<5, 0>;
+    case 6: return mana::k_mana_rowS<6, 1>;
+    case 7: return mana::k_mana_rowS<7, 2>;
+  }
+  return nullptr;
+}
+
+ColCFn colc_fn(int H, int S) {
+  if (H == 4 && S == 32) return mana::k_mana_colC<4, 32>;
+  if (H == 5 && S == 16) return mana::k_mana_colC<5, 16>;
+  if (H == 5 && S == 8) return mana::k_mana_colC<5, 8>;
+  if (H == 6 && S == 8) return mana::k_mana_colC<6, 8>;
+  if (H == 6 && S == 4) return mana::k_mana_colC<6, 4>;
+  if (H == 7 && S == 4) return mana::k_mana_colC<7, 4>;
+  if (H == 7 && S == 2) return mana::k_mana_colC<7, 2>;
+  return nullptr;
+}
 
 RowFn row_fn(int L, bool final_) {
   if (final_) {
@@ -385,7 +602,7 @@ RowFn row_fn(int L, bool final_) {
       case 5: return mana::k_mana_row<5, false>;
       case 6: return mana::k_mana_row<6, false>;
       case 7: return mana::k_mana_row<7, false>;
-      case 8: return mana::k_mana_row<8, false>;
+      case 8: return std::getenv("SRE_MANA_G2") ? mana::k_mana_row<8, false, 2> : mana::k_mana_row<8, false>;
     }
   }
   return nullptr;
@@ -393,9 +610,13 @@ RowFn row_fn(int L, bool final_) {
 
 ColFn col_fn(int H, int S) {
   if (H == 4 && S == 32) return mana::k_mana_col<4, 32>;
+  if (H == 4 && S == 16) return mana::k_mana_col<4, 16>;
   if (H == 5 && S == 16) return mana::k_mana_col<5, 16>;
+  if (H == 5 && S == 8) return mana::k_mana_col<5, 8>;
   if (H == 6 && S == 8) return mana::k_mana_col<6, 8>;
+  if (H == 6 && S == 4) return mana::k_mana_col<6, 4>;
   if (H == 7 && S == 4) return mana::k_mana_col<7, 4>;
+  if (H == 7 && S == 2) return mana::k_mana_col<7, 2>;
   if (H == 8 && S == 2) return mana::k_mana_col<8, 2>;
   return nullptr;
 }
@@ -444,6 +665,25 @@ int run_mana(const double2* psi, int N, uint64_t a_begin, uint64_t a_end, char* 
       for (uint64_t p0 = 0; p0 < pairs; p0 += (1u << 30)) {
         mana::RowArgs A{psi, nullptr, slots, a_begin, a_end, p0, (int)std::min<uint64_t>(pairs - p0, 1u << 30), 0};
         MCK(launch_counted(LK_SINGLE, st, [&] { f<<<g, kThreads, m.row_smem, st>>>(A); return cudaGetLastError(); }));
+      }
+    } else if (m.staged) {
+      uint64_t P = (ws_bytes - kSlotBytes) / m.row_bytes;
+      if (P > m.P) P = m.P;
+      if (P > pairs) P = pairs;
+      RowSFn fa = rows_fn(m.L);
+      ColCFn fb = colc_fn(m.H, m.S);
+      if (!fa || !fb) return fail(SRE_EINTERNAL, "no staged mana kernels for N=%d (L=%d H=%d S=%d)", N, m.L, m.H, m.S);
+      const int occA = occupancy((const void*)fa, m.row_smem), occB = occupancy((const void*)fb, m.col_smem);
+      const int nblk = (p3(m.L) + m.S - 1) / m.S;
+      for (uint64_t p0 = 0; p0 < pairs; p0 += P) {
+        const int np = (int)std::min<uint64_t>(P, pairs - p0);
+        const int PP = std::min(m.PP, np);
+        const int gA = grid_for((long)p3(m.H) * ((np + PP - 1) / PP), occA, d.sms);
+        const int gB = grid_for((long)np * nblk, occB, d.sms);
+        mana::RowSArgs A{psi, rows, a_begin, a_end, p0, np, m.H, m.S, PP};
+        mana::ColCArgs B{rows, slots, np, m.L};
+        MCK(launch_counted(LK_PASSA, st, [&] { fa<<<gA, kThreads, m.row_smem, st>>>(A); return cudaGetLastError(); }));
+        MCK(launch_counted(LK_PASSB, st, [&] { fb<<<gB, kThreads, m.col_smem, st>>>(B); return cudaGetLastError(); }));
       }
     } else {
       uint64_t P = (ws_bytes - kSlotBytes) / m.row_bytes;
