@@ -92,3 +92,55 @@ def mana(psi, mode: str = "fwht") -> float:
 def strange_mana() -> float:
     """Closed form for the strange state (|1> - |2>)/sqrt2: W = (1/3)(...) gives sum|W| = 5/3."""
     return math.log2(5.0 / 3.0)
+
+
+# ---------------------------------------------------------------------------------------------
+# Mixed states (NEXT-4): rho as a 3^N x 3^N array; passed to C column-major (Alg. 6's input).
+# ---------------------------------------------------------------------------------------------
+def _rho_prep(rho):
+    rho = np.asarray(rho, dtype=np.complex128)
+    if rho.ndim != 2 or rho.shape[0] != rho.shape[1]:
+        raise ValueError("rho must be a square 2-D array")
+    n = n_qutrits(rho.shape[0])
+    flat = np.ascontiguousarray(rho.flatten(order="F"))     # flat[r + c 3^N] = rho[r, c]
+    return flat, n
+
+
+def _mixed_lib():
+    lib = _lib()
+    dp = ctypes.POINTER(ctypes.c_double)
+    for f in (lib.oracle_mana_mixed_phase_space, lib.oracle_mana_mixed_alg6):
+        f.argtypes = [dp, ctypes.c_int, dp]
+        f.restype = ctypes.c_int
+    return lib
+
+
+def sums_mixed_phase_space(rho) -> np.ndarray:
+    """sum_u |Tr(rho A_u)|, sum_u Tr(rho A_u) from the definition (Eqs. (5)-(9)); N <= 4."""
+    flat, n = _rho_prep(rho)
+    out = np.zeros(2)
+    if _mixed_lib().oracle_mana_mixed_phase_space(_dp(flat.view(np.float64)), n, _dp(out)):
+        raise ValueError("oracle_mana_mixed_phase_space: N must be 1..4")
+    return out
+
+
+def sums_mixed_alg6(rho) -> np.ndarray:
+    """Alg. 6 literally (Vec_N + leg sweep with the dense 9x9 M); N <= 8."""
+    flat, n = _rho_prep(rho)
+    out = np.zeros(2)
+    if _mixed_lib().oracle_mana_mixed_alg6(_dp(flat.view(np.float64)), n, _dp(out)):
+        raise ValueError("oracle_mana_mixed_alg6: N must be 1..8")
+    return out
+
+
+def mana_mixed(rho, mode: str = "alg6") -> float:
+    rho = np.asarray(rho)
+    n = n_qutrits(rho.shape[0])
+    s = {"alg6": sums_mixed_alg6, "phase_space": sums_mixed_phase_space}[mode](rho)
+    return math.log2(s[0] / 3.0 ** n)
+
+
+def mixed_strange_mana(p: float) -> float:
+    """rho = p |S><S| + (1-p) I/3 (S the strange state): W(0) = (1-4p)/9, the other 8 points
+    (2+p)/18 each, so sum|W| = (7+8p)/9 for p >= 1/4 and 1 below."""
+    return math.log2(max(1.0, (7.0 + 8.0 * p) / 9.0))

@@ -494,3 +494,132 @@ int oracle_mana_fwht(const double* psi, int N, uint64_t a_lo, uint64_t a_hi, dou
   free(p3);
   return 0;
 }
+
+/* =============================================================================================
+ * Mixed-state qutrit mana (NEXT-4), Sec. 3.4 (Eq. (45), Alg. 6).
+ * rho: 3^N x 3^N complex128, column-major (rho[r + c 3^N] = <r|rho|c>), as Alg. 6 requires.
+ * sums[0] = sum_u |w_u|, sums[1] = sum_u Re w_u, w_u = Tr(rho A_u); mana = log2(sums[0] / 3^N)
+ * (Eq. (10); reading C18 for the 1/3^N); sums[1] = 3^N Tr(rho).
+ * ============================================================================================= */
+
+/* single-qutrit A_u, u = 3a + b, as a 3x3 matrix: Eqs. (5)-(7) with N = 1, dense. */
+static void qutrit_A1(C A[9][3][3]) {
+  C T1[9][3][3];
+  for (int a = 0; a < 3; a++)
+    for (int b = 0; b < 3; b++) {
+      C ph = w3(-2 * a * b);
+      for (int r = 0; r < 3; r++)
+        for (int c = 0; c < 3; c++) {
+          C val = {0.0L, 0.0L};
+          if (r == (c + b) % 3) val = cmul(ph, w3(a * r));
+          T1[3 * a + b][r][c] = val;
+        }
+    }
+  C A0[3][3];
+  memset(A0, 0, sizeof(A0));
+  for (int u = 0; u < 9; u++)
+    for (int r = 0; r < 3; r++)
+      for (int c = 0; c < 3; c++) { A0[r][c].re += T1[u][r][c].re / 3.0L; A0[r][c].im += T1[u][r][c].im / 3.0L; }
+  for (int u = 0; u < 9; u++) {
+    C t[3][3];
+    for (int r = 0; r < 3; r++)
+      for (int c = 0; c < 3; c++) {
+        C acc = {0.0L, 0.0L};
+        for (int k = 0; k < 3; k++) { C p = cmul(T1[u][r][k], A0[k][c]); acc.re += p.re; acc.im += p.im; }
+        t[r][c] = acc;
+      }
+    for (int r = 0; r < 3; r++)
+      for (int c = 0; c < 3; c++) {
+        C acc = {0.0L, 0.0L};
+        for (int k = 0; k < 3; k++) {
+          C td = {T1[u][c][k].re, -T1[u][c][k].im};
+          C p = cmul(t[r][k], td);
+          acc.re += p.re;
+          acc.im += p.im;
+        }
+        A[u][r][c] = acc;
+      }
+  }
+}
+
+/* Phase-space definition for rho: w_u = Tr(rho A_u) with A_u = (x)_j A_{u_j} (Eqs. (5)-(7); the
+ * N-qutrit A_u is the tensor product of single-qutrit ones because T_u and A_0 factorise).  Direct
+ * O(9^N * 9^N) double sum: N <= 4. */
+int oracle_mana_mixed_phase_space(const double* rho, int N, double* sums) {
+  if (N < 1 || N > 4) return 1;
+  const uint64_t D = pow3(N), U = D * D;
+  C A1[9][3][3];
+  qutrit_A1(A1);
+  R s_abs = 0.0L, s_sum = 0.0L;
+  for (uint64_t u = 0; u < U; u++) {
+    C w = {0.0L, 0.0L};
+    for (uint64_t r = 0; r < D; r++)
+      for (uint64_t c = 0; c < D; c++) {
+        /* Tr(rho A) = sum_{r,c} rho_{rc} A_{cr} */
+        C a = {1.0L, 0.0L};
+        uint64_t uu = u;
+        for (int j = 0; j < N; j++) {
+          a = cmul(a, A1[uu % 9][digit3(c, j)][digit3(r, j)]);
+          uu /= 9;
+        }
+        C rv = {rho[2 * (r + c * D)], rho[2 * (r + c * D) + 1]};
+        C p = cmul(rv, a);
+        w.re += p.re;
+        w.im += p.im;
+      }
+    s_abs += sqrtl(w.re * w.re + w.im * w.im);
+    s_sum += w.re;
+  }
+  sums[0] = (double)s_abs;
+  sums[1] = (double)s_sum;
+  return 0;
+}
+
+/* Alg. 6 literally: M_{u,:} = vec(A_u^T)^T (column-major vec), Vec_N with
+ * mu_k = 3 i_k + j_k and p = sum_k mu_k 9^{N-1-k} (i_k = ternary digit k of the row index r,
+ * j_k of the column index c; reading C19), then the in-place leg sweep with the dense 9x9 M. */
+int oracle_mana_mixed_alg6(const double* rho, int N, double* sums) {
+  if (N < 1 || N > 8) return 1;
+  const uint64_t D = pow3(N), V = D * D;
+  C A1[9][3][3];
+  qutrit_A1(A1);
+  C M[9][9];
+  for (int u = 0; u < 9; u++)
+    for (int al = 0; al < 9; al++) {
+      const int q = al % 3, p = al / 3;          /* column-major vec: alpha = q + 3p <-> (q, p) */
+      M[u][al] = A1[u][p][q];                    /* (A_u^T)_{qp} = (A_u)_{pq} */
+    }
+  C* v = (C*)malloc(sizeof(C) * V);
+  if (!v) return 2;
+  for (uint64_t c = 0; c < D; c++)
+    for (uint64_t r = 0; r < D; r++) {
+      uint64_t p = 0;
+      for (int k = 0; k < N; k++) p = 9 * p + (uint64_t)(3 * digit3(r, k) + digit3(c, k));
+      v[p].re = rho[2 * (r + c * D)];
+      v[p].im = rho[2 * (r + c * D) + 1];
+    }
+  for (int l = 0; l < N; l++) {
+    uint64_t ns = 1;
+    for (int k = 0; k < N - 1 - l; k++) ns *= 9;
+    const uint64_t bs = 9 * ns, nb = V / bs;
+#pragma omp parallel for schedule(static)
+    for (int64_t b = 0; b < (int64_t)nb; b++)
+      for (uint64_t m = 0; m < ns; m++) {
+        const uint64_t base = (uint64_t)b * bs + m;
+        C x[9], y[9];
+        for (int a = 0; a < 9; a++) x[a] = v[base + (uint64_t)a * ns];
+        for (int a = 0; a < 9; a++) {
+          y[a].re = 0.0L;
+          y[a].im = 0.0L;
+          for (int k = 0; k < 9; k++) { C pr = cmul(M[a][k], x[k]); y[a].re += pr.re; y[a].im += pr.im; }
+        }
+        for (int a = 0; a < 9; a++) v[base + (uint64_t)a * ns] = y[a];
+      }
+  }
+  R s_abs = 0.0L, s_sum = 0.0L;
+  for (uint64_t k = 0; k < V; k++) { s_abs += sqrtl(v[k].re * v[k].re + v[k].im * v[k].im); s_sum += v[k].re; }
+  free(v);
+  sums[0] = (double)s_abs;
+  sums[1] = (double)s_sum;
+  return 0;
+}

@@ -102,3 +102,32 @@ def clifford_circuit(psi, depth: int, rng):
         for k in range(0, n - 1, 2):
             psi = sum_gate(psi, int(perm[k]), int(perm[k + 1]))
     return psi
+
+
+def density(psi) -> np.ndarray:
+    """|psi><psi| as a 3^N x 3^N array (rho[r, c] = psi_r conj(psi_c))."""
+    return np.outer(psi, np.conj(psi))
+
+
+def reduced(psi, n_keep: int) -> np.ndarray:
+    """Tr_B |psi><psi| keeping qutrits 0..n_keep-1 (the low ternary digits; reading C21)."""
+    n = round(math.log(psi.size, 3))
+    phi = psi.reshape(3 ** (n - n_keep), 3 ** n_keep)        # phi[x_B, x_A]
+    return phi.T @ np.conj(phi)                                # rho[r, c] = sum_b phi[b,r] conj(phi[b,c])
+
+
+def mixed_strange(p: float) -> np.ndarray:
+    s = strange()
+    return p * np.outer(s, np.conj(s)) + (1.0 - p) * np.eye(3) / 3.0
+
+
+def random_mixed(n: int, rank: int, seed: int) -> np.ndarray:
+    """sum_k p_k |psi_k><psi_k| with Haar psi_k and Dirichlet weights p (rank <= 3^N)."""
+    rng = np.random.default_rng(seed)
+    p = rng.dirichlet(np.ones(rank))
+    rho = np.zeros((3 ** n, 3 ** n), dtype=np.complex128)
+    for k in range(rank):
+        v = rng.standard_normal(3 ** n) + 1j * rng.standard_normal(3 ** n)
+        v /= np.linalg.norm(v)
+        rho += p[k] * np.outer(v, np.conj(v))
+    return rho
