@@ -43,6 +43,14 @@ MANA_CONFIGS = {
     "m14": ("N=14 qutrit brick-wall state, depth 4 (pure-state mana, PAPER Table II row N=14, P:1449-1466)", 14, 4, 14014),
 }
 MANA_METRIC = "exact pure-state qutrit mana, phase-space points/s (9^N per state)"
+# Mixed-state qutrit mana (NEXT-4, Alg. 6): name -> (label, N_A kept qutrits, N total, depth, seed)
+MIXED_CONFIGS = {
+    "x8": ("rho_A of an N=10 qutrit brick-wall state (depth 3) on N_A=8 qutrits (PAPER P:1418-1430, Table II N_A=8)",
+           8, 10, 3, 10003),
+    "x10": ("rho_A of an N=12 qutrit brick-wall state (depth 4) on N_A=10 qutrits (PAPER Table II N_A=10, 56 GB)",
+            10, 12, 4, 12004),
+}
+MIXED_METRIC = "exact mixed-state qutrit mana, phase-space points/s (9^N_A per density matrix)"
 FP64_OPS_PER_CLK_SM = 64        # B200 FP64 pipe (measured 63.9/clk/SM, profiles/r01_microbench.json)
 
 
@@ -77,10 +85,13 @@ class Clocks:
                                       stdout=self.f, stderr=subprocess.DEVNULL)
         except OSError:
             self.p = None
+        self.t0 = time.time()
 
-    def stop(self):
+    def stop(self, min_seconds=0.5):
         if self.p is None:
             return None
+        if time.time() - self.t0 < min_seconds:      # short timed regions: let nvidia-smi take a sample
+            time.sleep(min_seconds - (time.time() - self.t0))
         self.p.terminate()
         self.p.wait()
         self.f.flush()
@@ -338,18 +349,177 @@ def main_mana(args):
     return 0
 
 
+def mixed_phi(cfg):
+    """Phi[x_B, x_A] of the config's pure state (rho_A = Phi^T conj(Phi), qutrits 0..N_A-1 kept)."""
+    import sre_inputs.qutrit as q
+    _, na, n, depth, seed = MIXED_CONFIGS[cfg]
+    return q.brickwall(n, depth, seed).reshape(3 ** (n - na), 3 ** na)
+
+
+def mixed_oracle_sample(seconds_hint=None):
+    """Oracle Alg. 6 (long double, OpenMP over fibers) on the x8 workload: the full transform is
+    not divisible into independent units, so the bounded sample is the whole N_A = 8 problem."""
+    import oracle
+    from oracle import mana as om
+    phi = mixed_phi("x8")
+    rho = phi.T @ np.conj(phi)
+    t0 = time.perf_counter()
+    om.sums_mixed_alg6(rho)
+    dt = time.perf_counter() - t0
+    return {"value": 9.0 ** 8 / dt, "unit": "phase-space points/s", "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"oracle Alg. 6 (long double, dense 9x9 leg sweep) on the full x8 problem "
+                      f"(N_A=8, 9^8 points) in {dt:.2f} s", "seconds": dt}
+
+
+def run_mixed_reference(args):
+    if int(os.environ.get("RANK", "0")) != 0:
+        return 0
+    label, na, n, depth, seed = MIXED_CONFIGS[args.config]
+    import oracle
+    oracle.build()
+    times = []
+    for i in range(args.warmup + args.steps):
+        cb = mixed_oracle_sample()
+        if i >= args.warmup:
+            times.append(cb["seconds"])
+    dt = sum(times)
+    value = args.steps * 9.0 ** 8 / dt
+    cb.update({"value": value})
+    print(json.dumps({
+        "impl": "reference", "metric": MIXED_METRIC, "value": value, "unit": "phase-space points/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64 (long double accum)",
+        "data": "synthetic", "config": {"workload": label, "N_A": na, "N": n, "depth": depth, "seed": seed,
+                                        "oracle_problem": "x8 (N_A=8) -- the whole transform is the smallest unit"},
+        "cpu_baseline": cb,
+        "e2e": {"value": value, "unit": "phase-space points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+    return 0
+
+
+def main_mixed(args):
+    """A step = Alg. 6 on one density matrix: the full leg sweep M^{(x)N_A} in place on the
+    column-major rho (fused multi-leg passes), the sums, and the host log2.  The input is
+    regenerated on the device (rho_A = Phi^H Phi, cuBLAS) before each step, outside the timed
+    region (the in-place transform consumes it).  Single GPU: the sweep has no X-string loop to
+    shard (replicas only)."""
+    import math
+
+    import torch
+
+    import paper_2601_07824_b200 as sre
+    from paper_2601_07824_b200 import qutrit
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    rank = int(os.environ.get("RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    label, na, n, depth, seed = MIXED_CONFIGS[args.config]
+    d = 3 ** na
+    phi = torch.from_numpy(mixed_phi(args.config)).to(dev)
+    flat = torch.empty(d * d, dtype=torch.complex128, device=dev)
+    out = torch.empty(2, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def regen():                                   # column-major rho: X[c, r] = rho[r, c] = (Phi^H Phi)[c, r]
+        torch.matmul(phi.conj().t(), phi, out=flat.view(d, d))
+
+    def step():
+        qutrit.mixed_sums_(flat, na, out=out, stream=stream)
+        h = out.cpu().numpy()
+        return math.log2(h[0] / d), h[1] / d
+
+    for _ in range(max(args.warmup, 0)):
+        regen()
+        m, tr = step()
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    launches0 = sre.launch_count()
+    sre.profile_begin(1)
+    step_ms = []
+    for _ in range(args.steps):
+        regen()                                    # > L2: the 9^N_A x 16 B input itself flushes L2
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        m, tr = step()
+        e1.record(stream)
+        e1.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+    prof = sre.profile_end()
+    launches = sre.launch_count() - launches0
+    clk = clocks.stop()
+    tot_ms = sum(step_ms)
+    pts = 9.0 ** na
+    value = args.steps * pts / (tot_ms * 1e-3)
+    # e2e: sre_mana_mixed from pinned host memory (H2D of the whole rho inside the timed region)
+    e2e = None
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = 0
+    nbytes = d * d * 16
+    if avail > 2.5 * nbytes:
+        regen()
+        host = torch.empty(d * d, dtype=torch.complex128, pin_memory=True)
+        host.copy_(flat)
+        del flat
+        torch.cuda.empty_cache()
+        t_e = []
+        for _ in range(2 if na <= 8 else 1):
+            t0 = time.perf_counter()
+            qutrit.mana_mixed(host)               # 1-D column-major flat: H2D + sweep + D2H
+            t_e.append(time.perf_counter() - t0)
+        e2e = {"value": pts * len(t_e) / sum(t_e), "unit": "phase-space points/s", "h2d_bytes_per_step": nbytes,
+               "d2h_bytes_per_step": 16, "ms_per_step": 1e3 * sum(t_e) / len(t_e)}
+    else:
+        e2e = {"value": None, "unit": "phase-space points/s", "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": 16,
+               "note": f"host has {avail / 2**30:.0f} GiB available, < 2.5 x {nbytes / 2**30:.0f} GiB needed"}
+    if rank != 0:
+        return 0
+    peaks, psrc = load_peaks()
+    kinds = {k: v for k, v in prof.items() if v["timed"] > 0 and k != "aux"}
+    share = {k: v["ms_sum"] / v["timed"] * v["launched"] for k, v in kinds.items()}
+    dom = max(share, key=share.get)
+    avg_ms = prof[dom]["ms_sum"] / prof[dom]["timed"]
+    bytes_launch = (2.0 if dom == "pass_a" else 1.0) * nbytes    # non-final pass: read + write; final: read
+    achieved = bytes_launch / (avg_ms * 1e-3) / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": achieved / peaks["hbm_gbs"], "traffic": None, "kernel": dom, "avg_launch_ms": avg_ms,
+            "launches_timed": prof[dom]["timed"], "share_of_step": share[dom] / tot_ms,
+            "bytes_per_launch": bytes_launch, "peak_source": psrc}
+    line = {
+        "metric": MIXED_METRIC, "value": value, "unit": "phase-space points/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": label, "N_A": na, "N": n, "depth": depth, "seed": seed,
+                   "l2": f"input ({nbytes / 2**20:.0f} MiB) larger than L2, regenerated before each step (untimed)",
+                   "step": "in-place fused leg sweep + sums + log2", "parallelism": "replicas only"},
+        "roofline": roof, "gpu_launches": int(launches), "clocks": clk, "e2e": e2e,
+        "result": {"mana": m, "trace": tr}, "profile": prof,
+    }
+    if not args.no_cpu_baseline:
+        import oracle
+        oracle.build()
+        line["cpu_baseline"] = mixed_oracle_sample()
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS) + sorted(MANA_CONFIGS))
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS) + sorted(MANA_CONFIGS) + sorted(MIXED_CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-stride", type=int, default=16)
     args = ap.parse_args()
     if args.config in MANA_CONFIGS:
         return run_mana_reference(args) if args.impl == "reference" else main_mana(args)
+    if args.config in MIXED_CONFIGS:
+        return run_mixed_reference(args) if args.impl == "reference" else main_mixed(args)
     if args.impl == "reference":
         return run_reference(args)
 

@@ -204,6 +204,37 @@ int sre_mana_partial_sums(const void* psi, int N, uint64_t a_begin, uint64_t a_e
  */
 int sre_mana(const void* psi, int N, double* out_mana, double* out_norm2);
 
+/* ============================================================================================
+ * Mixed-state qutrit mana (NEXT-4): Algorithm 6, Sec. 3.4 (Eq. (45)).
+ *
+ * rho: 3^N x 3^N complex128, COLUMN-MAJOR (rho[r + c 3^N] = <r|rho|c>, Alg. 6's input), 16-byte
+ * aligned; qutrit j = ternary digit j of r and c (DESIGN C19).  The library applies M^{(x)N}
+ * (w_u = Tr(rho A_u)) leg by leg and accumulates in FP64
+ *   S_abs = sum_u |w_u|      S_sum = sum_u w_u  ( = 3^N Tr rho ).
+ * Mana = log2(S_abs / 3^N) (Eq. (10), DESIGN C18/C20).  N in [1, SRE_MANA_MIXED_MAX_N]
+ * (N = 10 is 9^10 x 16 B = 56 GB of HBM).
+ * ============================================================================================ */
+#define SRE_MANA_MIXED_MAX_N 10
+
+/* Bytes of device workspace sre_mana_mixed_sums needs (per-CTA accumulator slots). */
+size_t sre_mana_mixed_workspace_size(int N);
+
+/*
+ * sre_mana_mixed_sums -- asynchronous, IN PLACE: rho (DEVICE pointer) is overwritten by w
+ * (transformed through all but the last leg; its contents are unspecified afterwards).
+ *   sums_dev : device double[2] <- (S_abs, S_sum).   stream: cudaStream_t (NULL = default).
+ * Errors: SRE_EINVAL (NULL / misaligned / host rho), SRE_ERANGE (N), SRE_EWORKSPACE, SRE_ECUDA.
+ */
+int sre_mana_mixed_sums(void* rho, int N, void* workspace, size_t ws_bytes, double* sums_dev, void* stream);
+
+/*
+ * sre_mana_mixed -- synchronous convenience; rho is a HOST or DEVICE pointer and is not modified
+ * (copied into a library-owned device buffer of 9^N x 16 bytes).
+ *   out_mana : log2(S_abs / 3^N).   out_trace (may be NULL): S_sum / 3^N = Tr rho.
+ * Returns SRE_ENOTNORM (out_trace set, out_mana untouched) when |Tr rho - 1| > 1e-8.
+ */
+int sre_mana_mixed(const void* rho, int N, double* out_mana, double* out_trace);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,470 @@
+// mana_mixed.cu -- mixed-state qutrit mana (NEXT-4): Algorithm 6 of PAPER.md on sm_100a.
+//
+// w = M^{(x)N} Vec_N(rho) (Eq. (45)), w_u = Tr(rho A_u), mana = log2(sum_u |w_u| / 3^N) (DESIGN C18,
+// C20).  The single-qutrit map M acts on the nine entries rho_{rc} of one leg as
+//     w_{(a,b)} = omega^{2ab} sum_r omega^{a r} rho_{r, 2b-r}
+// i.e. three 3-point DFTs on the lines r + c = 2b (the F_3 (+) F_3 (+) F_3 structure of P:971-982)
+// and a unit phase.  B200 design:
+//  * No Vec_N reorder: the leg sweep runs in place on the column-major rho the caller provides
+//    (rho[r + c 3^N]); leg k is the ternary digit pair (k, N + k) of the flat index.
+//  * HBM-bound (9^N complex128 = 56 GB at N = 10): several legs are fused per pass on a shared-
+//    memory tile of <= 6561 elements: pass 1 covers legs 0..3 (contiguous 81-element runs), later
+//    passes 3 legs each with 9 contiguous spectator elements (r digits 0, 1) per run.  N = 10
+//    therefore costs 3 HBM round trips instead of the 10 of a leg-by-leg sweep; the last pass
+//    accumulates sum |Re w| and sum Re w instead of storing w.
+//  * Persistent grids, per-CTA FP64 slots in launch order, a fixed-order reduction (deterministic).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "../../include/sre.h"
+#include "launch.cuh"
+
+namespace sre_host {
+int fail(int code, const char* fmt, ...);
+int get_dev(Dev& d);
+int is_device_ptr(const void* ptr, bool& dev);
+}  // namespace sre_host
+
+namespace mixed {
+
+__host__ __device__ constexpr long p3(int k) {
+  long r = 1;
+  for (int i = 0; i < k; ++i) r *= 3;
+  return r;
+}
+
+constexpr int kThreads = 256;
+constexpr int kSlots = 4096;
+constexpr double kC = 0.86602540378443864676;   // sqrt(3)/2
+
+__device__ __forceinline__ double2 mul_w(double2 v) {   // v * omega, omega = (-1/2, sqrt3/2)
+  return make_double2(fma(-0.5, v.x, -kC * v.y), fma(kC, v.x, -0.5 * v.y));
+}
+__device__ __forceinline__ double2 mul_w2(double2 v) {  // v * omega^2 = v * (-1/2, -sqrt3/2)
+  return make_double2(fma(-0.5, v.x, kC * v.y), fma(-kC, v.x, -0.5 * v.y));
+}
+
+// One leg: x[r][c] = rho_{rc} of the fiber -> x[a][b] = w_{(a,b)}.
+__device__ __forceinline__ void leg9(double2 (&x)[3][3]) {
+  double2 y[3][3];
+#pragma unroll
+  for (int b = 0; b < 3; ++b) {
+    const double2 x0 = x[0][(2 * b) % 3], x1 = x[1][(2 * b + 2) % 3], x2 = x[2][(2 * b + 1) % 3];
+    const double sr = x1.x + x2.x, si = x1.y + x2.y;
+    const double dr = x1.x - x2.x, di = x1.y - x2.y;
+    const double tr = fma(-0.5, sr, x0.x), ti = fma(-0.5, si, x0.y);
+    const double2 z0 = make_double2(x0.x + sr, x0.y + si);
+    const double2 z1 = make_double2(fma(-kC, di, tr), fma(kC, dr, ti));   // t + i c d
+    const double2 z2 = make_double2(fma(kC, di, tr), fma(-kC, dr, ti));   // t - i c d
+    y[0][b] = z0;
+    // a = 1: omega^{2b};  a = 2: omega^{4b} = omega^{b}
+    y[1][b] = (b == 0) ? z1 : (b == 1 ? mul_w2(z1) : mul_w(z1));
+    y[2][b] = (b == 0) ? z2 : (b == 1 ? mul_w(z2) : mul_w2(z2));
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) x[a][b] = y[a][b];
+}
+
+// Leg J of a tile with SP spectator digits and NL legs: tile element e = s + 3^SP (R + 3^NL C),
+// global element base + s + R sR + C sC.  LDG: the fiber is read from global memory (first leg),
+// STG: written to global memory (last leg of a non-final pass), ACC: accumulated (last leg of the
+// final pass); otherwise shared memory.
+template <int SP, int NL, int J, bool LDG, bool STG, bool ACC>
+__device__ __forceinline__ void leg_stage(double2* tile, double2* g, long base, long sR, long sC, double& aa,
+                                          double& as) {
+  constexpr int S3 = (int)p3(SP), R3 = (int)p3(NL), PJ = (int)p3(J), PH = (int)p3(NL - 1 - J);
+  constexpr int sr = S3 * PJ, sc = S3 * R3 * PJ;
+  constexpr int fibers = S3 * (int)p3(NL - 1) * (int)p3(NL - 1);
+  const long gr = PJ * sR, gc = PJ * sC;
+#pragma unroll 2
+  for (int f = threadIdx.x; f < fibers; f += kThreads) {
+    int q = f;
+    const int s = q % S3;
+    q /= S3;
+    int rlo, rhi;
+    if constexpr (SP == 0 && J == 1) {   // stride-9 fibers first: 8 consecutive threads hit 8 banks
+      rhi = q % PH;
+      q /= PH;
+      rlo = q % PJ;
+      q /= PJ;
+    } else {
+      rlo = q % PJ;
+      q /= PJ;
+      rhi = q % PH;
+      q /= PH;
+    }
+    const int clo = q % PJ;
+    q /= PJ;
+    const int chi = q;
+    const int tb = s + S3 * (rlo + PJ * 3 * rhi + R3 * (clo + PJ * 3 * chi));
+    const long gb = base + s + (long)(rlo + PJ * 3 * rhi) * sR + (long)(clo + PJ * 3 * chi) * sC;
+    double2 x[3][3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        if constexpr (LDG) x[r][c] = __ldcs(g + gb + r * gr + c * gc);
+        else x[r][c] = tile[tb + r * sr + c * sc];
+      }
+    leg9(x);
+    if constexpr (ACC) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+          aa += fabs(x[a][b].x);
+          as += x[a][b].x;
+        }
+    } else {
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+          if constexpr (STG) __stcs(g + gb + a * gr + b * gc, x[a][b]);
+          else tile[tb + a * sr + b * sc] = x[a][b];
+        }
+    }
+  }
+}
+
+template <int SP, int NL, int J, bool FINAL>
+__device__ __forceinline__ void leg_stages(double2* tile, double2* g, long base, long sR, long sC, double& aa,
+                                           double& as) {
+  if constexpr (J < NL) {
+    constexpr bool first = (J == 0), last = (J == NL - 1);
+    leg_stage<SP, NL, J, first, last && !FINAL, last && FINAL>(tile, g, base, sR, sC, aa, as);
+    __syncthreads();
+    leg_stages<SP, NL, J + 1, FINAL>(tile, g, base, sR, sC, aa, as);
+  }
+}
+
+__device__ __forceinline__ void flush(double aa, double as, double* slots) {
+  __shared__ double red[2][kThreads / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    aa += __shfl_down_sync(0xffffffffu, aa, o);
+    as += __shfl_down_sync(0xffffffffu, as, o);
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    red[0][w] = aa;
+    red[1][w] = as;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double ta = 0.0, ts = 0.0;
+    for (int i = 0; i < kThreads / 32; ++i) {
+      ta += red[0][i];
+      ts += red[1][i];
+    }
+    slots[2 * blockIdx.x] += ta;
+    slots[2 * blockIdx.x + 1] += ts;
+  }
+}
+
+struct LegArgs {
+  double2* rho;         // column-major 3^N x 3^N, transformed in place
+  double* slots;
+  int N;
+  int k0;               // first leg of this pass
+  long items;           // 9^N / (3^SP 9^NL)
+};
+
+// One pass: legs k0 .. k0+NL-1 on tiles of 3^SP x 9^NL elements.  Free digits (the item index,
+// fastest first): r digits [SP, k0), r digits [k0+NL, N), c digits [0, k0), c digits [k0+NL, N).
+template <int SP, int NL, bool FINAL>
+__global__ void __launch_bounds__(kThreads) k_legs(LegArgs A) {
+  constexpr int S3 = (int)p3(SP);
+  extern __shared__ double2 tile[];
+  const int N = A.N, k0 = A.k0;
+  const long nrl = p3(k0 - SP), nrh = p3(N - k0 - NL), ncl = p3(k0);
+  const long sR = p3(k0), sC = p3(N + k0);
+  const long pRH = p3(k0 + NL), pCL = p3(N), pCH = p3(N + k0 + NL);
+  double aa = 0.0, as = 0.0;
+  if constexpr (NL == 1) {       // one leg: no tile, every thread owns one fiber of some item
+    const long nf = A.items * S3;
+    for (long F = (long)blockIdx.x * kThreads + threadIdx.x; F < nf; F += (long)gridDim.x * kThreads) {
+      const long s = F % S3;
+      long x = F / S3;
+      const long rl = x % nrl;
+      x /= nrl;
+      const long rh = x % nrh;
+      x /= nrh;
+      const long cl = x % ncl;
+      x /= ncl;
+      const long gb = s + rl * S3 + rh * pRH + cl * pCL + x * pCH;
+      double2 v[3][3];
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) v[r][c] = __ldcs(A.rho + gb + r * sR + c * sC);
+      leg9(v);
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+          if constexpr (FINAL) {
+            aa += fabs(v[a][b].x);
+            as += v[a][b].x;
+          } else {
+            __stcs(A.rho + gb + a * sR + b * sC, v[a][b]);
+          }
+        }
+    }
+  } else {
+    for (long it = blockIdx.x; it < A.items; it += gridDim.x) {
+      long x = it;
+      const long rl = x % nrl;
+      x /= nrl;
+      const long rh = x % nrh;
+      x /= nrh;
+      const long cl = x % ncl;
+      x /= ncl;
+      const long base = rl * S3 + rh * pRH + cl * pCL + x * pCH;
+      leg_stages<SP, NL, 0, FINAL>(tile, A.rho, base, sR, sC, aa, as);   // ends with __syncthreads
+    }
+  }
+  if constexpr (FINAL) flush(aa, as, A.slots);
+}
+
+__global__ void __launch_bounds__(256) k_mixed_reduce(const double* slots, int n, double* out) {
+  __shared__ double sa[256], ss[256];
+  double a = 0.0, s = 0.0;
+  for (int i = threadIdx.x; i < n; i += 256) {
+    a += slots[2 * i];
+    s += slots[2 * i + 1];
+  }
+  sa[threadIdx.x] = a;
+  ss[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) {
+      sa[threadIdx.x] += sa[threadIdx.x + o];
+      ss[threadIdx.x] += ss[threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out[0] = sa[0];
+    out[1] = ss[0];
+  }
+}
+
+}  // namespace mixed
+
+// ==========================================================================================
+// host
+// ==========================================================================================
+namespace {
+using namespace sre_host;
+using mixed::kSlots;
+using mixed::kThreads;
+
+#define XCK(x)                                                                                \
+  do {                                                                                        \
+    cudaError_t e_ = (x);                                                                     \
+    if (e_ != cudaSuccess) return fail(SRE_ECUDA, "%s: %s (%s:%d)", #x, cudaGetErrorString(e_), \
+                                       __FILE__, __LINE__);                                   \
+  } while (0)
+
+constexpr size_t kSlotBytes = (size_t)kSlots * 2 * sizeof(double);
+
+struct Pass {
+  int SP, NL, k0;
+};
+
+// Default: legs 0..3 on contiguous 81 x 81 tiles, then 3 legs per pass with 9 spectators.
+// SRE_MIXED_PLAN="SP:NL,SP:NL,..." overrides (experiments).
+std::vector<Pass> make_passes(int N) {
+  std::vector<Pass> v;
+  const char* e = std::getenv("SRE_MIXED_PLAN");
+  if (e) {
+    int k0 = 0;
+    const char* p = e;
+    while (*p && k0 < N) {
+      int sp = 0, nl = 0, used = 0;
+      if (std::sscanf(p, "%d:%d%n", &sp, &nl, &used) != 2) break;
+      const bool ok = nl >= 1 && nl <= 4 && sp >= 0 && sp <= 4 && sp <= k0 && mixed::p3(sp) * mixed::p3(2 * nl) <= 6561;
+      if (!ok) break;
+      v.push_back({sp, nl, k0});
+      k0 += nl;
+      p += used;
+      if (*p == ',') ++p;
+    }
+    if (k0 == N) return v;
+    v.clear();
+  }
+  // measured on B200: after the 81 x 81 pass, 3-leg passes with 9-element
+  // runs; a remainder of 1, 2 or 4 legs goes to 27-element-run passes (a read-only final pass
+  // with 27-element runs is 2x faster than one with 9-element runs).
+  const int first = N < 4 ? N : 4;
+  v.push_back({0, first, 0});
+  int k0 = first;
+  int rem = N - k0;
+  while (rem > 0) {
+    const int nl = (rem == 4 || rem == 2) ? 2 : (rem >= 3 ? 3 : 1);
+    v.push_back({nl == 3 ? 2 : 3, nl, k0});
+    k0 += nl;
+    rem -= nl;
+  }
+  return v;
+}
+
+using LegFn = void (*)(mixed::LegArgs);
+
+template <bool F>
+LegFn leg_fn_t(int sp, int nl) {
+  switch (sp * 10 + nl) {
+    case 1: return mixed::k_legs<0, 1, F>;
+    case 2: return mixed::k_legs<0, 2, F>;
+    case 3: return mixed::k_legs<0, 3, F>;
+    case 4: return mixed::k_legs<0, 4, F>;
+    case 21: return mixed::k_legs<2, 1, F>;
+    case 22: return mixed::k_legs<2, 2, F>;
+    case 23: return mixed::k_legs<2, 3, F>;
+    case 31: return mixed::k_legs<3, 1, F>;
+    case 32: return mixed::k_legs<3, 2, F>;
+    case 41: return mixed::k_legs<4, 1, F>;
+    case 42: return mixed::k_legs<4, 2, F>;
+  }
+  return nullptr;
+}
+LegFn leg_fn(int sp, int nl, bool fin) { return fin ? leg_fn_t<true>(sp, nl) : leg_fn_t<false>(sp, nl); }
+
+int occupancy(const void* fn, size_t smem) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, int>> seen;
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& s : seen)
+    if (s.first == fn) return s.second;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, smem) != cudaSuccess || occ < 1) occ = 1;
+  cudaGetLastError();
+  seen.push_back({fn, occ});
+  return occ;
+}
+
+int run_mixed(double2* rho, int N, char* ws, size_t ws_bytes, double* sums_dev, cudaStream_t st) {
+  Dev d;
+  int rc = get_dev(d);
+  if (rc) return rc;
+  if (ws_bytes < kSlotBytes) return fail(SRE_EWORKSPACE, "workspace %zu < required %zu", ws_bytes, kSlotBytes);
+  double* slots = reinterpret_cast<double*>(ws);
+  XCK(cudaMemsetAsync(slots, 0, kSlotBytes, st));
+  const std::vector<Pass> passes = make_passes(N);
+  for (size_t i = 0; i < passes.size(); ++i) {
+    const Pass& p = passes[i];
+    const bool fin = (i + 1 == passes.size());
+    LegFn f = leg_fn(p.SP, p.NL, fin);
+    if (!f || p.k0 < p.SP) return fail(SRE_EINTERNAL, "no leg kernel for SP=%d NL=%d k0=%d", p.SP, p.NL, p.k0);
+    const long E = mixed::p3(p.SP) * mixed::p3(2 * p.NL);
+    const size_t smem = p.NL == 1 ? 0 : (size_t)E * sizeof(double2);
+    const long items = mixed::p3(2 * N) / E;
+    const long work = p.NL == 1 ? (items * mixed::p3(p.SP) + kThreads - 1) / kThreads : items;
+    long g = (long)occupancy((const void*)f, smem) * d.sms;
+    if (g > work) g = work;
+    if (g > kSlots) g = kSlots;
+    mixed::LegArgs A{rho, slots, N, p.k0, items};
+    const int grid = (int)g;
+    XCK(launch_counted(fin ? LK_PASSB : LK_PASSA, st, [&] { f<<<grid, kThreads, smem, st>>>(A); return cudaGetLastError(); }));
+  }
+  XCK(launch_counted(LK_AUX, st, [&] { mixed::k_mixed_reduce<<<1, 256, 0, st>>>(slots, kSlots, sums_dev); return cudaGetLastError(); }));
+  return SRE_OK;
+}
+
+struct XCache {
+  std::mutex mu;
+  char* buf = nullptr;
+  size_t bytes = 0;
+  int dev = -1;
+};
+XCache g_xcache;
+
+uint64_t pow3u(int n) {
+  uint64_t r = 1;
+  for (int i = 0; i < n; ++i) r *= 3;
+  return r;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t sre_mana_mixed_workspace_size(int N) {
+  if (N < 1 || N > SRE_MANA_MIXED_MAX_N) return 0;
+  return kSlotBytes;
+}
+
+int sre_mana_mixed_sums(void* rho, int N, void* workspace, size_t ws_bytes, double* sums_dev, void* stream) {
+  if (!rho) return fail(SRE_EINVAL, "rho is NULL");
+  if (N < 1 || N > SRE_MANA_MIXED_MAX_N) return fail(SRE_ERANGE, "N=%d outside [1, %d]", N, SRE_MANA_MIXED_MAX_N);
+  if (!workspace) return fail(SRE_EINVAL, "workspace is NULL");
+  if (!sums_dev) return fail(SRE_EINVAL, "sums_dev is NULL");
+  if (reinterpret_cast<uintptr_t>(rho) % 16) return fail(SRE_EINVAL, "rho not 16-byte aligned");
+  bool dv = false;
+  int rc = is_device_ptr(rho, dv);
+  if (rc) return rc;
+  if (!dv) return fail(SRE_EINVAL, "rho must be a device pointer");
+  return run_mixed(reinterpret_cast<double2*>(rho), N, reinterpret_cast<char*>(workspace), ws_bytes, sums_dev,
+                   reinterpret_cast<cudaStream_t>(stream));
+}
+
+int sre_mana_mixed(const void* rho, int N, double* out_mana, double* out_trace) {
+  if (!rho) return fail(SRE_EINVAL, "rho is NULL");
+  if (N < 1 || N > SRE_MANA_MIXED_MAX_N) return fail(SRE_ERANGE, "N=%d outside [1, %d]", N, SRE_MANA_MIXED_MAX_N);
+  if (!out_mana) return fail(SRE_EINVAL, "out_mana is NULL");
+  if (reinterpret_cast<uintptr_t>(rho) % 16) return fail(SRE_EINVAL, "rho not 16-byte aligned");
+  Dev d;
+  int rc = get_dev(d);
+  if (rc) return rc;
+  bool dev_ptr = false;
+  rc = is_device_ptr(rho, dev_ptr);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lk(g_xcache.mu);
+  if (g_xcache.dev != d.id) {
+    g_xcache.buf = nullptr;
+    g_xcache.bytes = 0;
+    g_xcache.dev = d.id;
+  }
+  const uint64_t D = pow3u(N);
+  const size_t vbytes = (size_t)(D * D) * sizeof(double2);
+  const size_t need = vbytes + kSlotBytes + 256;
+  if (g_xcache.bytes < need) {
+    if (g_xcache.buf) cudaFree(g_xcache.buf);
+    g_xcache.buf = nullptr;
+    g_xcache.bytes = 0;
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&g_xcache.buf), need);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(SRE_ENOMEM, "cudaMalloc(%zu): %s", need, cudaGetErrorString(e));
+    }
+    g_xcache.bytes = need;
+  }
+  cudaStream_t st = 0;
+  double2* v = reinterpret_cast<double2*>(g_xcache.buf);
+  XCK(cudaMemcpyAsync(v, rho, vbytes, dev_ptr ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+  char* ws = g_xcache.buf + vbytes;
+  double* sums = reinterpret_cast<double*>(ws + kSlotBytes);
+  rc = run_mixed(v, N, ws, kSlotBytes, sums, st);
+  if (rc) return rc;
+  double hs[2];
+  XCK(cudaMemcpyAsync(hs, sums, sizeof(hs), cudaMemcpyDeviceToHost, st));
+  XCK(cudaStreamSynchronize(st));
+  const double tr = hs[1] / (double)D;   // sum_u Tr(rho A_u) = 3^N Tr(rho)
+  if (out_trace) *out_trace = tr;
+  if (!(std::fabs(tr - 1.0) <= 1e-8)) return fail(SRE_ENOTNORM, "Tr(rho) = %.17g", tr);
+  *out_mana = std::log2(hs[0] / (double)D);
+  return SRE_OK;
+}
+
+}  // extern "C"

@@ -3,6 +3,8 @@
 
     m, norm2 = mana(psi)                       # P:869-884 Alg. 5; log2(sum |chi| / 3^N), Eq. (10)
     sums = partial_sums(psi, a0, a1)           # device [2] = (sum |chi|, sum chi) over X-strings [a0, a1)
+    m, tr = mana_mixed(rho)                    # P:1059-1087 Alg. 6 (mixed states, NEXT-4)
+    sums = mixed_sums_(rho_flat_cuda, n)       # in place: rho overwritten; device [2] = (sum |w|, sum w)
 
 psi: complex128 of length 3^N (qutrit j = ternary digit j of the index), numpy or torch.
 """
@@ -28,6 +30,12 @@ def _lib():
         lib.sre_mana_partial_sums.restype = i
         lib.sre_mana.argtypes = [vp, i, dp, dp]
         lib.sre_mana.restype = i
+        lib.sre_mana_mixed_workspace_size.argtypes = [i]
+        lib.sre_mana_mixed_workspace_size.restype = ctypes.c_size_t
+        lib.sre_mana_mixed_sums.argtypes = [vp, i, vp, ctypes.c_size_t, vp, vp]
+        lib.sre_mana_mixed_sums.restype = i
+        lib.sre_mana_mixed.argtypes = [vp, i, dp, dp]
+        lib.sre_mana_mixed.restype = i
         _ready = True
     return lib
 
@@ -92,4 +100,64 @@ def partial_sums(psi, a_begin: int, a_end: int, out=None, workspace=None, stream
                                      ctypes.c_void_p(workspace.data_ptr()), workspace.numel(),
                                      ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(st.cuda_stream)))
     del keep
+    return out
+
+
+def _mixed_flat(rho):
+    """(pointer, N, keepalive) of a column-major flat complex128 buffer (rho[r + c 3^N]).
+    2-D inputs are transposed into column-major order; 1-D inputs are taken as already flat."""
+    try:
+        import torch
+        if isinstance(rho, torch.Tensor):
+            if rho.dtype != torch.complex128:
+                raise SreError(1, "rho must be complex128")
+            t = rho.t().contiguous() if rho.dim() == 2 else rho.contiguous()
+            d = rho.shape[0] if rho.dim() == 2 else int(round(t.numel() ** 0.5))
+            return t.data_ptr(), n_qutrits(d), t
+    except ImportError:
+        pass
+    a = np.asarray(rho)
+    if a.dtype != np.complex128:
+        raise SreError(1, "rho must be complex128")
+    if a.ndim == 2:
+        if a.shape[0] != a.shape[1]:
+            raise SreError(1, "rho must be square")
+        d = a.shape[0]
+        a = np.ascontiguousarray(a.flatten(order="F"))
+    else:
+        a = np.ascontiguousarray(a)
+        d = int(round(a.size ** 0.5))
+    return a.ctypes.data, n_qutrits(d), a
+
+
+def mana_mixed(rho):
+    """(mana, Tr rho) of a density matrix (host or cuda; 2-D, or 1-D column-major flat) via
+    sre_mana_mixed (Alg. 6; synchronous; rho is not modified)."""
+    lib = _lib()
+    ptr, n, keep = _mixed_flat(rho)
+    m = ctypes.c_double(0.0)
+    tr = ctypes.c_double(0.0)
+    _check(lib.sre_mana_mixed(ctypes.c_void_p(ptr), n, ctypes.byref(m), ctypes.byref(tr)))
+    del keep
+    return m.value, tr.value
+
+
+def mixed_sums_(rho_flat, n: int, out=None, workspace=None, stream=None):
+    """IN PLACE on a cuda column-major flat rho (length 9^n): device float64[2] = (sum |w_u|,
+    sum w_u); rho's contents are unspecified afterwards.  Enqueued on ``stream``."""
+    import torch
+    lib = _lib()
+    if not (isinstance(rho_flat, torch.Tensor) and rho_flat.is_cuda and rho_flat.is_contiguous()):
+        raise SreError(1, "mixed_sums_ needs a contiguous cuda complex128 tensor")
+    if rho_flat.numel() != 9 ** n:
+        raise SreError(2, f"rho has {rho_flat.numel()} entries, 9^{n} expected")
+    dev = rho_flat.device
+    if out is None:
+        out = torch.empty(2, dtype=torch.float64, device=dev)
+    need = int(lib.sre_mana_mixed_workspace_size(n))
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=dev)
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    _check(lib.sre_mana_mixed_sums(ctypes.c_void_p(rho_flat.data_ptr()), n, ctypes.c_void_p(workspace.data_ptr()),
+                                   workspace.numel(), ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(st.cuda_stream)))
     return out
