@@ -253,7 +253,8 @@ def main_mana(args):
         dist.init_process_group("nccl", device_id=dev)
     label, n, depth, seed = MANA_CONFIGS[args.config]
     na = 3 ** n
-    lo, hi = na * rank // world, na * (rank + 1) // world
+    from paper_2601_07824_b200.dist import shard_bounds
+    lo, hi = shard_bounds(na, rank, world)              # contiguous X-string shard
     psi_host = mana_state(args.config)
     psi = torch.from_numpy(psi_host).to(dev)
     ws = torch.empty(qutrit.workspace_size(n), dtype=torch.uint8, device=dev)

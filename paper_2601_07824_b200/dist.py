@@ -51,3 +51,47 @@ def exact(psi, alphas: Sequence[float] = (2.0,), group=None, workspace=None):
             dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
 
     return exact_sharded(n, alphas, rank, world, part, allreduce, lambda s: finalize(s, n, alphas))
+
+
+# ---------------------------------------------------------------------------------------------
+# Pure-state qutrit mana (NEXT-3): the same structure over the 3^N X-strings of Alg. 5 (its loop
+# over a is as independent as Alg. 2's), two sums (sum |chi|, sum chi) per state.
+# Mixed-state mana (Alg. 6) has no X-string loop and runs as replicas.
+# ---------------------------------------------------------------------------------------------
+def shard_bounds(total: int, rank: int, world: int):
+    """Contiguous, equal shard [lo, hi) of `total` units for rank `rank` of `world`."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"rank {rank} / world {world}")
+    return rank * total // world, (rank + 1) * total // world
+
+
+def mana_sharded(n: int, rank: int, world: int, partial_fn: Callable, allreduce_fn: Callable):
+    """partial_fn(lo, hi) -> [2] sums over X-strings [lo, hi) of 3^n; allreduce_fn sums them in
+    place over ranks.  Returns (mana = log2(sum|chi| / 3^n), ||psi||^2 = sum chi / 3^n)."""
+    import math
+    lo, hi = shard_bounds(3 ** n, rank, world)
+    sums = partial_fn(lo, hi)
+    allreduce_fn(sums)
+    s = [float(x) for x in sums.cpu().reshape(-1)] if hasattr(sums, "cpu") else [float(x) for x in sums]
+    return math.log2(s[0] / 3 ** n), s[1] / 3 ** n
+
+
+def mana(psi, group=None, workspace=None):
+    """Pure-state qutrit mana of psi (cuda complex128 [3^N], identical on every rank) using every
+    rank of `group`; returns (mana, ||psi||^2) on all ranks."""
+    import torch.distributed as dist
+
+    from . import qutrit
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    n = qutrit.n_qutrits(psi.numel())
+
+    def part(lo, hi):
+        return qutrit.partial_sums(psi, lo, hi, workspace=workspace)
+
+    def allreduce(t):
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+
+    return mana_sharded(n, rank, world, part, allreduce)

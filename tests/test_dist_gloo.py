@@ -77,3 +77,53 @@ def test_shard_plan_partitions():
             assert all(rs[i][1] == rs[i + 1][0] for i in range(world - 1))
             sizes = [b - a for a, b in rs]
             assert max(sizes) - min(sizes) <= 1
+
+
+def _mana_worker(rank, world, port, n, out_q):
+    import torch.distributed as dist
+
+    from oracle import mana as om
+    from paper_2601_07824_b200 import dist as sdist
+    import sre_inputs.qutrit as sq
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    psi = sq.brickwall(n, 3, 778)
+
+    def part(lo, hi):
+        return torch.from_numpy(om.sums_fwht(psi, (lo, hi)))
+
+    def allreduce(t):
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+
+    m, n2 = sdist.mana_sharded(n, rank, world, part, allreduce)
+    out_q.put((rank, m, n2))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_mana_sharded_equals_single(world):
+    """NEXT-3 shards: 3^N X-strings split over ranks, one all_reduce of the two sums."""
+    import torch.multiprocessing as mp
+
+    from oracle import mana as om
+    import sre_inputs.qutrit as sq
+    from paper_2601_07824_b200 import dist as sdist
+    n = 5
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_mana_worker, args=(r, world, port, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    ref = om.mana(sq.brickwall(n, 3, 778))
+    for _, m, n2 in res:
+        assert m == pytest.approx(ref, abs=1e-12) and n2 == pytest.approx(1.0, abs=1e-12)
+    bounds = [sdist.shard_bounds(3 ** n, r, world) for r in range(world)]
+    assert bounds[0][0] == 0 and bounds[-1][1] == 3 ** n
+    assert all(bounds[i][1] == bounds[i + 1][0] for i in range(world - 1))
