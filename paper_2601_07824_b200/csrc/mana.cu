@@ -20,6 +20,7 @@
 //    fixed-order reduction: results are bitwise reproducible for a given device and N.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -222,7 +223,7 @@ struct RowArgs {
 
 // Pass A / single pass.  Row h of pair p: w_l = v1_{h,l} + i v2_{h,l}, F_3 over the L low digits.
 template <int L, bool FINAL, int G = (L > 5 ? L - 5 : 0)>
-__global__ void __launch_bounds__(kThreads, 2) k_mana_row(RowArgs A) {
+__global__ void __launch_bounds__(kThreads) k_mana_row(RowArgs A) {
   // G: low digits done in registers (3^G consecutive l per thread group)
   constexpr int RG = p3(G);
   constexpr int NT = p3(L - G);              // thread groups per row
@@ -341,19 +342,80 @@ struct RowSArgs {
   int PP;               // pairs per item
 };
 
-template <int L, int G>
+// Digit-shift tables of one X-string's low digits: for ternary digit j of an index k,
+//   sub(k) = sum_j ds[j][k_j],  neg(k) = sum_j dn[j][k_j]   with
+//   ds[j][d] = ((d - a_j) mod 3) 3^j,  dn[j][d] = ((-d - a_j) mod 3) 3^j.
+// Built once per X-string; an unrolled loop over compile-time k then needs two adds per index.
+template <int G>
+struct ShiftTab {
+  int ds[G > 0 ? G : 1][3], dn[G > 0 ? G : 1][3];
+  __device__ __forceinline__ void build(int a) {
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      const int aj = a % 3, p = p3(j);
+      a /= 3;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        ds[j][d] = ((d - aj + 3) % 3) * p;
+        dn[j][d] = ((6 - d - aj) % 3) * p;
+      }
+    }
+  }
+};
+
+// Two-digit (G = 2) generator with compile-time shifts: both X-strings of a pair whose low parts
+// are C and C + 1 (mod 9, no carry into digit 2) read the same two 9-blocks bA (rowA) and bB
+// (rowB); the digit shifts are then compile-time permutations of registers.
+__host__ __device__ constexpr int sub2(int i, int c) {
+  return ((i % 3 - c % 3 + 3) % 3) + 3 * ((i / 3 - c / 3 + 3) % 3);
+}
+__host__ __device__ constexpr int neg2(int i, int c) {
+  return ((6 - i % 3 - c % 3) % 3) + 3 * ((6 - i / 3 - c / 3) % 3);
+}
+template <int C>
+__device__ __forceinline__ void gen9(const double2 (&bA)[9], const double2 (&bB)[9], double2 (&r)[9], bool two) {
+#pragma unroll
+  for (int i = 0; i < 9; ++i) {
+    const double2 x1 = bA[sub2(i, C)], x2 = bB[neg2(i, C)];
+    double2 w;
+    w.x = x1.x * x2.x + x1.y * x2.y;
+    w.y = x1.x * x2.y - x1.y * x2.x;
+    if (two) {
+      const double2 y1 = bA[sub2(i, C + 1)], y2 = bB[neg2(i, C + 1)];
+      w.x -= y1.x * y2.y - y1.y * y2.x;
+      w.y += y1.x * y2.x + y1.y * y2.y;
+    }
+    r[i] = w;
+  }
+}
+
+// Staged pass A.  Template S = workspace column-block width (compile-time: the store index
+// l -> (l / S, l % S) is a shift).  Per thread: the 3^G consecutive l of group t; per pair the
+// shift tables of the two X-strings' low digits, and the shifted upper digits of t.
+template <int L, int G, int S>
 __global__ void __launch_bounds__(kThreads) k_mana_rowS(RowSArgs A) {
   constexpr int RG = p3(G);
   constexpr int NT = p3(L - G);
   constexpr int NL = p3(L);
+  constexpr int NBLK = (NL + S - 1) / S;
+  static_assert(NT <= kThreads, "one thread group per thread");
   extern __shared__ double2 smem[];
   double2* rowA = smem;            // psi row (h - a_hi)
   double2* rowB = smem + NL;       // psi row (-h - a_hi)
   double2* tile = smem + 2 * NL;
   const int nh = p3(A.H);
   const int nchunk = (A.npairs + A.PP - 1) / A.PP;
-  const int nblk = (NL + A.S - 1) / A.S;
   const long items = (long)nh * nchunk;
+  const int t = threadIdx.x;
+  int td[L - G > 0 ? L - G : 1];     // ternary digits of this thread's group index
+  {
+    int x = t;
+#pragma unroll
+    for (int j = 0; j < L - G; ++j) {
+      td[j] = x % 3;
+      x /= 3;
+    }
+  }
   for (long it = blockIdx.x; it < items; it += gridDim.x) {
     const int h = (int)(it / nchunk), ch = (int)(it % nchunk);
     const int p_lo = ch * A.PP, p_hi = min(A.npairs, p_lo + A.PP);
@@ -381,30 +443,76 @@ __global__ void __launch_bounds__(kThreads) k_mana_rowS(RowSArgs A) {
       const bool staged2 = (ah2 == ah1);
       int g2s = 0, g2n = 0;                   // rows for a2 when it crosses an a_hi boundary
       if (two && !staged2) tshift_rt(h, ah2, A.H, g2s, g2n);
-      for (int t = threadIdx.x; t < NT; t += kThreads) {
+      if (t < NT) {
+        // upper digits: (t - a_up) and (-t - a_up) digit-wise, from the precomputed digits of t
+        int us1 = 0, un1 = 0, us2 = 0, un2 = 0;
+        {
+          int b1 = al1 / RG, b2 = al2 / RG;
+#pragma unroll
+          for (int j = 0; j < L - G; ++j) {
+            const int c1 = b1 % 3, c2 = b2 % 3, p = p3(j);
+            b1 /= 3;
+            b2 /= 3;
+            us1 += ((td[j] - c1 + 3) % 3) * p;
+            un1 += ((6 - td[j] - c1) % 3) * p;
+            us2 += ((td[j] - c2 + 3) % 3) * p;
+            un2 += ((6 - td[j] - c2) % 3) * p;
+          }
+        }
+        ShiftTab<G> T1, T2;
+        T1.build(al1 % RG);
+        T2.build(al2 % RG);
+        const int oA1 = us1 * RG, oB1 = un1 * RG, oA2 = us2 * RG, oB2 = un2 * RG;
         double2 r[RG];
-        int us1, un1, us2, un2;
-        tshift<L - G>(t, al1 / RG, us1, un1);
-        tshift<L - G>(t, al2 / RG, us2, un2);
+        bool done = false;
+        if constexpr (G == 2) {
+          const int c = al1 % 9;
+          if (c != 8) {                        // a2's 9-blocks are a1's: one load per block element
+            double2 bA[9], bB[9];
+#pragma unroll
+            for (int k = 0; k < 9; ++k) {
+              bA[k] = rowA[oA1 + k];
+              bB[k] = rowB[oB1 + k];
+            }
+            switch (c) {
+              case 0: gen9<0>(bA, bB, r, two); break;
+              case 1: gen9<1>(bA, bB, r, two); break;
+              case 2: gen9<2>(bA, bB, r, two); break;
+              case 3: gen9<3>(bA, bB, r, two); break;
+              case 4: gen9<4>(bA, bB, r, two); break;
+              case 5: gen9<5>(bA, bB, r, two); break;
+              case 6: gen9<6>(bA, bB, r, two); break;
+              default: gen9<7>(bA, bB, r, two); break;
+            }
+            done = true;
+          }
+        }
 #pragma unroll
         for (int i = 0; i < RG; ++i) {
-          int ss, sn;
-          tshift<G>(i, al1 % RG, ss, sn);
-          double2 x1 = rowA[us1 * RG + ss];
-          double2 x2 = rowB[un1 * RG + sn];
+          if (done) break;
+          int ss1 = 0, sn1 = 0, ss2 = 0, sn2 = 0;
+#pragma unroll
+          for (int j = 0; j < G; ++j) {
+            const int dj = (i / p3(j)) % 3;   // compile-time digit of i
+            ss1 += T1.ds[j][dj];
+            sn1 += T1.dn[j][dj];
+            ss2 += T2.ds[j][dj];
+            sn2 += T2.dn[j][dj];
+          }
+          double2 x1 = rowA[oA1 + ss1];
+          double2 x2 = rowB[oB1 + sn1];
           double2 w;
-          w.x = x1.x * x2.x + x1.y * x2.y;
+          w.x = x1.x * x2.x + x1.y * x2.y;        // conj(alpha_x) alpha_{-x}
           w.y = x1.x * x2.y - x1.y * x2.x;
           if (two) {
-            tshift<G>(i, al2 % RG, ss, sn);
             if (staged2) {
-              x1 = rowA[us2 * RG + ss];
-              x2 = rowB[un2 * RG + sn];
-            } else {
-              x1 = __ldg(A.psi + (size_t)g2s * NL + us2 * RG + ss);
-              x2 = __ldg(A.psi + (size_t)g2n * NL + un2 * RG + sn);
+              x1 = rowA[oA2 + ss2];
+              x2 = rowB[oB2 + sn2];
+            } else {                               // a2 crosses an a_hi boundary (1 pair in 3^L / 2)
+              x1 = __ldg(A.psi + (size_t)g2s * NL + oA2 + ss2);
+              x2 = __ldg(A.psi + (size_t)g2n * NL + oB2 + sn2);
             }
-            w.x -= x1.x * x2.y - x1.y * x2.x;   // + i v2
+            w.x -= x1.x * x2.y - x1.y * x2.x;      // + i v2
             w.y += x1.x * x2.x + x1.y * x2.y;
           }
           r[i] = w;
@@ -414,14 +522,13 @@ __global__ void __launch_bounds__(kThreads) k_mana_rowS(RowSArgs A) {
         for (int i = 0; i < RG; ++i) tile[t * RG + i] = r[i];
       }
       __syncthreads();
-      double2* dst = A.ws + (size_t)pl * ((size_t)nblk * nh * A.S) + (size_t)h * A.S;
-      const int S = A.S, bs = nh * A.S;
+      double2* dst = A.ws + (size_t)pl * ((size_t)NBLK * nh * S) + (size_t)h * S;
+      const size_t bs = (size_t)nh * S;
       auto to_ws = [&](int l, double2 v) {     // last stage: straight to the column-blocked workspace
-        const int cb = l / S;
-        __stcg(dst + (size_t)cb * bs + (l - cb * S), v);
+        __stcg(dst + (size_t)(l / S) * bs + (l % S), v);
       };
-      auto no_ld = [&](int e) { return tile[e]; };
-      stages_f<L, 1, G, false>(tile, no_ld, to_ws);
+      auto from_tile = [&](int e) { return tile[e]; };
+      stages_f<L, 1, G, false>(tile, from_tile, to_ws);
       __syncthreads();
     }
   }
@@ -550,11 +657,14 @@ void make_mplan(int N, MPlan& m) {
   if (m.single) {
     m.P = 0;
   } else {
-    // L2-resident workspace (64 MiB) while a pair's transform is small; from 16 MiB per pair on
-    // the workspace streams through HBM anyway, so 8 pairs share each staged psi row.
-    uint64_t P = m.row_bytes >= (16ull << 20) ? 8 : (64ull << 20) / m.row_bytes;
+    // ~2 GiB of pairs per launch pair (measured: an L2-resident 64 MiB batch
+    // loses more to launch tails than it gains in L2 hits; HBM has room for the larger batch).
+    uint64_t P = (2ull << 30) / m.row_bytes;
+    if (P < 8) P = 8;
+    if (const char* e = std::getenv("SRE_MANA_P")) P = (uint64_t)std::atoll(e);   // experiments
     m.P = P < 1 ? 1 : (P > 4096 ? 4096 : P);
     m.PP = m.staged ? 8 : 1;
+    if (const char* e = std::getenv("SRE_MANA_PP")) m.PP = std::max(1, std::atoi(e));
   }
 }
 
@@ -565,11 +675,17 @@ using ColFn = void (*)(mana::ColArgs);
 using RowSFn = void (*)(mana::RowSArgs);
 using ColCFn = void (*)(mana::ColCArgs);
 
-RowSFn rows_fn(int L) {
-  switch (L) {
-    case 5: return mana::k_mana_rowS<5, 0>;
-    case 6: return mana::k_mana_rowS<6, 1>;
-    case 7: return mana::k_mana_rowS<7, 2>;
+RowSFn rows_fn(int L, int S) {
+  switch (L * 100 + S) {
+    case 532: return mana::k_mana_rowS<5, 0, 32>;
+    case 516: return mana::k_mana_rowS<5, 0, 16>;
+    case 632: return mana::k_mana_rowS<6, 1, 32>;
+    case 616: return mana::k_mana_rowS<6, 1, 16>;
+    case 608: return mana::k_mana_rowS<6, 1, 8>;
+    case 716: return mana::k_mana_rowS<7, 2, 16>;
+    case 708: return mana::k_mana_rowS<7, 2, 8>;
+    case 704: return mana::k_mana_rowS<7, 2, 4>;
+    case 702: return mana::k_mana_rowS<7, 2, 2>;
   }
   return nullptr;
 }
@@ -670,7 +786,7 @@ int run_mana(const double2* psi, int N, uint64_t a_begin, uint64_t a_end, char* 
       uint64_t P = (ws_bytes - kSlotBytes) / m.row_bytes;
       if (P > m.P) P = m.P;
       if (P > pairs) P = pairs;
-      RowSFn fa = rows_fn(m.L);
+      RowSFn fa = rows_fn(m.L, m.S);
       ColCFn fb = colc_fn(m.H, m.S);
       if (!fa || !fb) return fail(SRE_EINTERNAL, "no staged mana kernels for N=%d (L=%d H=%d S=%d)", N, m.L, m.H, m.S);
       const int occA = occupancy((const void*)fa, m.row_smem), occB = occupancy((const void*)fb, m.col_smem);
