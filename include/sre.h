@@ -179,8 +179,9 @@ int sre_profile_end(double* ms_sum, uint64_t* n_timed, uint64_t* n_launched);
  * ============================================================================================ */
 #define SRE_MANA_MAX_N 16
 
-/* Bytes of device workspace sre_mana_partial_sums needs for N (0 if N is out of range).  Less
- * is accepted down to the size of one X-string pair; fewer pairs then run per launch. */
+/* Bytes of device workspace sre_mana_partial_sums prefers for N (0 if N is out of range): about
+ * 2 GiB of X-string pairs per launch for N >= 9 (64 KiB for N <= 8).  Less is accepted down to
+ * the size of one X-string pair; fewer pairs then run per launch (slower, same result). */
 size_t sre_mana_workspace_size(int N);
 
 /*
