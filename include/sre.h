@@ -181,7 +181,8 @@ int sre_profile_end(double* ms_sum, uint64_t* n_timed, uint64_t* n_launched);
 
 /* Bytes of device workspace sre_mana_partial_sums prefers for N (0 if N is out of range): about
  * 2 GiB of X-string pairs per launch for N >= 9 (64 KiB for N <= 8).  Less is accepted down to
- * the size of one X-string pair; fewer pairs then run per launch (slower, same result). */
+ * the size of one X-string pair; fewer pairs then run per launch (slower; equal up to FP64
+ * reassociation). */
 size_t sre_mana_workspace_size(int N);
 
 /*
