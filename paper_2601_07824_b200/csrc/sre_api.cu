@@ -87,8 +87,13 @@ bool tmem_enabled() {  // opt-in (SRE_TMEM=1): the 4-warp TMEM pass B measured s
 
 int staged_groups(int N) {
   const char* e = getenv("SRE_KG");
-  if (e && atoi(e) > 0) return atoi(e) > 64 ? 64 : atoi(e);
-  return 8;  // 64 X-strings per launch pair (N=20: 512 MiB, measured faster than L2-sized 128 MiB: 4.07 vs 4.28 s)
+  if (e && atoi(e) > 0) return atoi(e) > 1024 ? 1024 : atoi(e);
+  // 8-X-string groups per staged launch pair, measured on B200: launch tails
+  // dominate small batches, so N <= 18 takes 4096 X-strings per launch (<= 8 GiB of workspace);
+  // N = 19 saturates at 512, N = 20 peaks at 128 (1 GiB).
+  if (N <= 18) return 512;
+  if (N == 19) return 64;
+  return 16;
 }
 
 void two_pass_params(int T, int& L, int& H, int& CB) {
@@ -120,7 +125,9 @@ int pick_gx(uint64_t count, int per_cta, int B, int resident) {
   return bg;
 }
 
-int make_plan(int N, const Dev& d, Plan& p) {
+// count: X-strings the call will evaluate (the staged batch never exceeds it, so short ranges and
+// single X-strings -- sre_x_string_sums, sre_chi, Monte-Carlo energies -- keep small slot arrays).
+int make_plan(int N, const Dev& d, Plan& p, uint64_t count = ~0ull) {
   p.N = N;
   p.T = N - 1;
   if (p.T <= SMALL_MAX_T) {
@@ -144,6 +151,14 @@ int make_plan(int N, const Dev& d, Plan& p) {
     const uint64_t itemsB = (uint64_t)p.K * 2 * (1ull << (p.L - p.CB));
     p.slots = (size_t)((itemsB + p.unitsB - 1) / p.unitsB);
     if (N >= 21 && N <= 25) {  // streamed pass A (k_passAs) + TMA-fed pass B with 2^13-double tiles
+      if (const char* e = getenv("SRE_K")) {   // experiments: X-strings per streamed launch pair
+        const int kk = atoi(e);
+        if (kk >= 8 && kk <= 512) {
+          p.K = kk;
+          p.slab_doubles = (size_t)p.K << N;
+          p.slots = (size_t)(((uint64_t)p.K * 2 * (1ull << (p.L - p.CB)) + p.unitsB - 1) / p.unitsB);
+        }
+      }
       p.staged = true;
       p.KG = 1;
       p.amin = 1ull << p.L;
@@ -152,6 +167,7 @@ int make_plan(int N, const Dev& d, Plan& p) {
     if (p.L == 10) {  // staged pass A + persistent pass B (N = 15..20)
       p.staged = true;
       p.KG = staged_groups(N);
+      if ((uint64_t)8 * p.KG > count) p.KG = (int)((count + 7) / 8 > 0 ? (count + 7) / 8 : 1);
       if ((size_t)8 * p.KG > (size_t)p.K) {
         p.K = 8 * p.KG;
         p.slab_doubles = (size_t)p.K << N;
@@ -212,6 +228,7 @@ std::vector<Sweep> make_sweeps(const double* alpha, int n_alpha) {
       } else {
         s.al.kind[i] = 2;
         s.al.iexp[i] = 0;
+        s.al.any_real = 1;
       }
       s.scale4[i] = std::pow(4.0, a);  // t = 4 t'  =>  t^alpha = 4^alpha t'^alpha
     }
@@ -345,7 +362,7 @@ int run_range(const double2* psi, int N, int B, uint64_t a_begin, uint64_t a_end
   int rc = get_dev(d);
   if (rc) return rc;
   Plan p;
-  make_plan(N, d, p);
+  make_plan(N, d, p, a_end - a_begin);
   if (ws_bytes < ws_bytes_for(p, B, prec))
     return fail(SRE_EWORKSPACE, "workspace %zu < required %zu", ws_bytes, ws_bytes_for(p, B, prec));
   if (prec == SRE_FP32) {
@@ -618,7 +635,7 @@ int sre_chi(const void* psi, int N, uint64_t a, double* chi_dev, void* stream) {
   rc = get_dev(d);
   if (rc) return rc;
   Plan p;
-  make_plan(N, d, p);
+  make_plan(N, d, p, 1);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const double2* dpsi = reinterpret_cast<const double2*>(psi);
   Alphas al;

@@ -32,6 +32,7 @@ constexpr int NACC = MAXA + 2;   // [0,MAXA) alpha sums, [MAXA] purity, [MAXA+1]
 struct Alphas {
   int n;                // alphas in this sweep
   int need_log;         // any alpha == 1
+  int any_real;         // any kind == 2 (non-integer alpha)
   int kind[MAXA];       // 0: integer exponent iexp[i] >= 1, 2: general real power
   int iexp[MAXA];
   double alpha[MAXA];
@@ -156,14 +157,13 @@ struct Epi {
     } else {
 #pragma unroll
       for (int i = 0; i < MAXA; ++i) {
-        if (i < al.n) {
-          if (al.kind[i] == 0) {
-            R pw = t;
-            for (int k = 1; k < al.iexp[i]; ++k) pw *= t;
-            acc[i] += pw;
-          } else {
-            acc[i] += (t > R(0)) ? exp(R(al.alpha[i]) * log(t)) : R(0);
-          }
+        if (i >= al.n) break;            // uniform: stop after the requested alphas
+        if (al.kind[i] == 0) {
+          R pw = t;
+          for (int k = 1; k < al.iexp[i]; ++k) pw *= t;
+          acc[i] += pw;
+        } else {
+          acc[i] += (t > R(0)) ? exp(R(al.alpha[i]) * log(t)) : R(0);
         }
       }
       if (al.need_log) acc[MAXA + 1] += (t > R(0)) ? t * log(t) : R(0);
@@ -173,13 +173,54 @@ struct Epi {
 
 // Epilogue of one tile's 32 values per thread into a fresh local sum, then one add into the
 // long-lived accumulators: keeps the running-sum chains ~32x shorter (DESIGN "Summation").
-template <bool A2, class R>
-__device__ __forceinline__ void tile_accumulate(double (&acc)[NACC], const R (&v)[32], const Alphas& al) {
+// General alphas run in three compact phases (integer powers + purity; t ln t if some alpha = 1;
+// real powers if some alpha is non-integer): interleaving the rarely-taken exp/log blocks with
+// the common path made the executed code sparse in a ~200 KB body (10x slower, I-cache bound).
+template <bool A2, class R, int M>
+__device__ __forceinline__ void tile_accumulate(double (&acc)[NACC], const R (&v)[M], const Alphas& al) {
   R loc[NACC];          // FP32 mode: 32-term local sums in FP32, one conversion per tile
 #pragma unroll
   for (int i = 0; i < NACC; ++i) loc[i] = R(0);
+  if constexpr (A2) {
 #pragma unroll
-  for (int j = 0; j < 32; ++j) Epi<A2, R>::add(loc, v[j], al);
+    for (int j = 0; j < M; ++j) Epi<true, R>::add(loc, v[j], al);
+  } else {
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+      const R t = v[j] * v[j];
+      loc[MAXA] += t;
+#pragma unroll
+      for (int i = 0; i < MAXA; ++i) {
+        if (i >= al.n) break;
+        if (al.kind[i] == 0) {
+          R pw = t;
+          for (int k = 1; k < al.iexp[i]; ++k) pw *= t;
+          loc[i] += pw;
+        }
+      }
+    }
+    if (al.need_log) {
+#pragma unroll
+      for (int j = 0; j < M; ++j) {
+        const R t = v[j] * v[j];
+        loc[MAXA + 1] += (t > R(0)) ? t * log(t) : R(0);
+      }
+    }
+    if (al.any_real) {
+#pragma unroll
+      for (int i = 0; i < MAXA; ++i) {
+        if (i >= al.n) break;
+        if (al.kind[i] != 0) {
+          const R a = R(al.alpha[i]);
+#pragma unroll 4
+          for (int j = 0; j < M; ++j) {
+            const R t = v[j] * v[j];
+            loc[i] += (t > R(0)) ? exp(a * log(t)) : R(0);
+          }
+        }
+      }
+    }
+  }
 #pragma unroll
   for (int i = 0; i < NACC; ++i) acc[i] += (double)loc[i];
 }
@@ -301,8 +342,10 @@ __global__ void __launch_bounds__(256) k_small(const typename Cx<V>::T* __restri
           chi_store(chi, a, p, 1, (uint64_t)g + (uint64_t)G * j, B[j]);
         }
       } else {
-#pragma unroll
-        for (int j = 0; j < R; ++j) { Epi<A2>::add(acc, (double)A[j], al); Epi<A2>::add(acc, (double)B[j], al); }
+        {
+          tile_accumulate<A2>(acc, A, al);
+          tile_accumulate<A2>(acc, B, al);
+        }
       }
     }
   }

@@ -12,14 +12,15 @@ import sre_inputs as si  # noqa: E402
 n, a0, cnt = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3])
 reps = int(sys.argv[4]) if len(sys.argv) > 4 else 2
 prec = sys.argv[5] if len(sys.argv) > 5 else "fp64"
+alphas = [float(x) for x in sys.argv[6].split(",")] if len(sys.argv) > 6 else [2.0]
 psi = torch.from_numpy(si.haar(n, 1234)).cuda()
-ws = torch.empty(sre.workspace_size(n, 1, 1, prec), dtype=torch.uint8, device="cuda")
-out = sre.partial_sums(psi, a0, a0 + cnt, [2.0], workspace=ws, precision=prec)
+ws = torch.empty(sre.workspace_size(n, 1, len(alphas), prec), dtype=torch.uint8, device="cuda")
+out = sre.partial_sums(psi, a0, a0 + cnt, alphas, workspace=ws, precision=prec)
 torch.cuda.synchronize()
 sre.profile_begin(1)
 t0 = time.perf_counter()
 for _ in range(reps):
-    out = sre.partial_sums(psi, a0, a0 + cnt, [2.0], workspace=ws, precision=prec)
+    out = sre.partial_sums(psi, a0, a0 + cnt, alphas, workspace=ws, precision=prec)
 torch.cuda.synchronize()
 dt = (time.perf_counter() - t0) / reps
 prof = sre.profile_end()
