@@ -185,9 +185,15 @@ __device__ __forceinline__ void tile_accumulate(double (&acc)[NACC], const R (&v
 #pragma unroll
     for (int j = 0; j < M; ++j) Epi<true, R>::add(loc, v[j], al);
   } else {
+    // General alphas: one compact (not unrolled) loop over the tile, t values staged through a
+    // per-thread local array (L1).  Unrolling 32 copies of log / exp(a log t) made the kernel
+    // instruction-cache bound (ncu: "no_instruction" the top stall).
+    R tv[M];
 #pragma unroll
+    for (int j = 0; j < M; ++j) tv[j] = v[j] * v[j];
+#pragma unroll 1
     for (int j = 0; j < M; ++j) {
-      const R t = v[j] * v[j];
+      const R t = tv[j];
       loc[MAXA] += t;
 #pragma unroll
       for (int i = 0; i < MAXA; ++i) {
@@ -196,29 +202,11 @@ __device__ __forceinline__ void tile_accumulate(double (&acc)[NACC], const R (&v
           R pw = t;
           for (int k = 1; k < al.iexp[i]; ++k) pw *= t;
           loc[i] += pw;
+        } else {
+          loc[i] += (t > R(0)) ? exp(R(al.alpha[i]) * log(t)) : R(0);
         }
       }
-    }
-    if (al.need_log) {
-#pragma unroll
-      for (int j = 0; j < M; ++j) {
-        const R t = v[j] * v[j];
-        loc[MAXA + 1] += (t > R(0)) ? t * log(t) : R(0);
-      }
-    }
-    if (al.any_real) {
-#pragma unroll
-      for (int i = 0; i < MAXA; ++i) {
-        if (i >= al.n) break;
-        if (al.kind[i] != 0) {
-          const R a = R(al.alpha[i]);
-#pragma unroll 4
-          for (int j = 0; j < M; ++j) {
-            const R t = v[j] * v[j];
-            loc[i] += (t > R(0)) ? exp(a * log(t)) : R(0);
-          }
-        }
-      }
+      if (al.need_log) loc[MAXA + 1] += (t > R(0)) ? t * log(t) : R(0);
     }
   }
 #pragma unroll
