@@ -145,3 +145,17 @@ def test_errors(qm):
                                      ws.numel(), ctypes.c_void_p(out.data_ptr()), None) == 2
     assert lib.sre_mana_partial_sums(ctypes.c_void_p(buf.data_ptr()), 4, 0, 81, ctypes.c_void_p(ws.data_ptr()),
                                      100, ctypes.c_void_p(out.data_ptr()), None) == 4
+
+
+@pytest.mark.parametrize("n", [1, 5, 9, 12])
+def test_empty_and_single_ranges(qm, n):
+    """Degenerate ranges: [a, a) gives zero sums; [a, a+1) (a lone, unpaired X-string) matches the
+    oracle for X-strings at the start, middle and end of [0, 3^N) on every path family."""
+    from oracle import mana as om
+    import sre_inputs.qutrit as q
+    psi = q.haar(n, 700 + n)
+    d = _cuda(psi)
+    z = qm.partial_sums(d, 3 ** n // 2, 3 ** n // 2).cpu().numpy()
+    assert np.array_equal(z, np.zeros(2))
+    for a in (0, 3 ** n // 2, 3 ** n - 1):
+        np.testing.assert_allclose(qm.partial_sums(d, a, a + 1).cpu().numpy(), om.sums_fwht(psi, (a, a + 1)), rtol=RTOL)
