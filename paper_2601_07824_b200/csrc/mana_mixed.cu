@@ -78,7 +78,7 @@ __device__ __forceinline__ void leg9(double2 (&x)[3][3]) {
 // global element base + s + R sR + C sC.  LDG: the fiber is read from global memory (first leg),
 // STG: written to global memory (last leg of a non-final pass), ACC: accumulated (last leg of the
 // final pass); otherwise shared memory.
-template <int SP, int NL, int J, bool LDG, bool STG, bool ACC>
+template <int SP, int NL, int J, bool LDG, bool STG, bool ACC, int NT>
 __device__ __forceinline__ void leg_stage(double2* tile, double2* g, long base, long sR, long sC, double& aa,
                                           double& as) {
   constexpr int S3 = (int)p3(SP), R3 = (int)p3(NL), PJ = (int)p3(J), PH = (int)p3(NL - 1 - J);
@@ -86,7 +86,7 @@ __device__ __forceinline__ void leg_stage(double2* tile, double2* g, long base, 
   constexpr int fibers = S3 * (int)p3(NL - 1) * (int)p3(NL - 1);
   const long gr = PJ * sR, gc = PJ * sC;
 #pragma unroll 2
-  for (int f = threadIdx.x; f < fibers; f += kThreads) {
+  for (int f = threadIdx.x; f < fibers; f += NT) {
     int q = f;
     const int s = q % S3;
     q /= S3;
@@ -136,19 +136,19 @@ __device__ __forceinline__ void leg_stage(double2* tile, double2* g, long base, 
   }
 }
 
-template <int SP, int NL, int J, bool FINAL>
+template <int SP, int NL, int J, bool FINAL, int NT>
 __device__ __forceinline__ void leg_stages(double2* tile, double2* g, long base, long sR, long sC, double& aa,
                                            double& as) {
   if constexpr (J < NL) {
     constexpr bool first = (J == 0), last = (J == NL - 1);
-    leg_stage<SP, NL, J, first, last && !FINAL, last && FINAL>(tile, g, base, sR, sC, aa, as);
+    leg_stage<SP, NL, J, first, last && !FINAL, last && FINAL, NT>(tile, g, base, sR, sC, aa, as);
     __syncthreads();
-    leg_stages<SP, NL, J + 1, FINAL>(tile, g, base, sR, sC, aa, as);
+    leg_stages<SP, NL, J + 1, FINAL, NT>(tile, g, base, sR, sC, aa, as);
   }
 }
 
 __device__ __forceinline__ void flush(double aa, double as, double* slots) {
-  __shared__ double red[2][kThreads / 32];
+  __shared__ double red[2][16];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     aa += __shfl_down_sync(0xffffffffu, aa, o);
@@ -162,7 +162,7 @@ __device__ __forceinline__ void flush(double aa, double as, double* slots) {
   __syncthreads();
   if (threadIdx.x == 0) {
     double ta = 0.0, ts = 0.0;
-    for (int i = 0; i < kThreads / 32; ++i) {
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
       ta += red[0][i];
       ts += red[1][i];
     }
@@ -181,8 +181,8 @@ struct LegArgs {
 
 // One pass: legs k0 .. k0+NL-1 on tiles of 3^SP x 9^NL elements.  Free digits (the item index,
 // fastest first): r digits [SP, k0), r digits [k0+NL, N), c digits [0, k0), c digits [k0+NL, N).
-template <int SP, int NL, bool FINAL>
-__global__ void __launch_bounds__(kThreads) k_legs(LegArgs A) {
+template <int SP, int NL, bool FINAL, int NT = kThreads>
+__global__ void __launch_bounds__(NT) k_legs(LegArgs A) {
   constexpr int S3 = (int)p3(SP);
   extern __shared__ double2 tile[];
   const int N = A.N, k0 = A.k0;
@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(kThreads) k_legs(LegArgs A) {
   double aa = 0.0, as = 0.0;
   if constexpr (NL == 1) {       // one leg: no tile, every thread owns one fiber of some item
     const long nf = A.items * S3;
-    for (long F = (long)blockIdx.x * kThreads + threadIdx.x; F < nf; F += (long)gridDim.x * kThreads) {
+    for (long F = (long)blockIdx.x * NT + threadIdx.x; F < nf; F += (long)gridDim.x * NT) {
       const long s = F % S3;
       long x = F / S3;
       const long rl = x % nrl;
@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(kThreads) k_legs(LegArgs A) {
       const long cl = x % ncl;
       x /= ncl;
       const long base = rl * S3 + rh * pRH + cl * pCL + x * pCH;
-      leg_stages<SP, NL, 0, FINAL>(tile, A.rho, base, sR, sC, aa, as);   // ends with __syncthreads
+      leg_stages<SP, NL, 0, FINAL, NT>(tile, A.rho, base, sR, sC, aa, as);   // ends with __syncthreads
     }
   }
   if constexpr (FINAL) flush(aa, as, A.slots);
@@ -338,9 +338,12 @@ LegFn leg_fn_t(int sp, int nl) {
   }
   return nullptr;
 }
-LegFn leg_fn(int sp, int nl, bool fin) { return fin ? leg_fn_t<true>(sp, nl) : leg_fn_t<false>(sp, nl); }
+LegFn leg_fn(int sp, int nl, bool fin, int threads) {
+  if (threads == 512 && sp == 0 && nl == 4) return fin ? mixed::k_legs<0, 4, true, 512> : mixed::k_legs<0, 4, false, 512>;
+  return fin ? leg_fn_t<true>(sp, nl) : leg_fn_t<false>(sp, nl);
+}
 
-int occupancy(const void* fn, size_t smem) {
+int occupancy(const void* fn, size_t smem, int threads) {
   static std::mutex mu;
   static std::vector<std::pair<const void*, int>> seen;
   std::lock_guard<std::mutex> lk(mu);
@@ -348,7 +351,7 @@ int occupancy(const void* fn, size_t smem) {
     if (s.first == fn) return s.second;
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int occ = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, smem) != cudaSuccess || occ < 1) occ = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem) != cudaSuccess || occ < 1) occ = 1;
   cudaGetLastError();
   seen.push_back({fn, occ});
   return occ;
@@ -365,18 +368,23 @@ int run_mixed(double2* rho, int N, char* ws, size_t ws_bytes, double* sums_dev, 
   for (size_t i = 0; i < passes.size(); ++i) {
     const Pass& p = passes[i];
     const bool fin = (i + 1 == passes.size());
-    LegFn f = leg_fn(p.SP, p.NL, fin);
+    int threads = kThreads;
+    if (p.SP == 0 && p.NL == 4) {
+      const char* e = std::getenv("SRE_MIXED_T0");   // experiments: threads of the 81 x 81 pass
+      if (e && std::atoi(e) == 512) threads = 512;
+    }
+    LegFn f = leg_fn(p.SP, p.NL, fin, threads);
     if (!f || p.k0 < p.SP) return fail(SRE_EINTERNAL, "no leg kernel for SP=%d NL=%d k0=%d", p.SP, p.NL, p.k0);
     const long E = mixed::p3(p.SP) * mixed::p3(2 * p.NL);
     const size_t smem = p.NL == 1 ? 0 : (size_t)E * sizeof(double2);
     const long items = mixed::p3(2 * N) / E;
-    const long work = p.NL == 1 ? (items * mixed::p3(p.SP) + kThreads - 1) / kThreads : items;
-    long g = (long)occupancy((const void*)f, smem) * d.sms;
+    const long work = p.NL == 1 ? (items * mixed::p3(p.SP) + threads - 1) / threads : items;
+    long g = (long)occupancy((const void*)f, smem, threads) * d.sms;
     if (g > work) g = work;
     if (g > kSlots) g = kSlots;
     mixed::LegArgs A{rho, slots, N, p.k0, items};
     const int grid = (int)g;
-    XCK(launch_counted(fin ? LK_PASSB : LK_PASSA, st, [&] { f<<<grid, kThreads, smem, st>>>(A); return cudaGetLastError(); }));
+    XCK(launch_counted(fin ? LK_PASSB : LK_PASSA, st, [&] { f<<<grid, threads, smem, st>>>(A); return cudaGetLastError(); }));
   }
   XCK(launch_counted(LK_AUX, st, [&] { mixed::k_mixed_reduce<<<1, 256, 0, st>>>(slots, kSlots, sums_dev); return cudaGetLastError(); }));
   return SRE_OK;
