@@ -285,11 +285,11 @@ int run_range_t(const typename Cx<V>::T* psi, const Plan& p, const Dev& d, int N
       CK(cudaMemsetAsync(partial, 0, sizeof(double) * (size_t)gx * B * NACC, st));
       cudaError_t e;
       if (p.kind == SMALL)
-        e = sw.a2 ? launch_small<V, true, false>(p.T, psi, N, B, gx, a_begin, count, sw.al, partial, nullptr, st)
-                  : launch_small<V, false, false>(p.T, psi, N, B, gx, a_begin, count, sw.al, partial, nullptr, st);
+        e = sw.a2 ? launch_small<V, true, false>(p.T, psi, N, B, gx, a_begin, count, sw.al, partial, nullptr, st, nullptr)
+                  : launch_small<V, false, false>(p.T, psi, N, B, gx, a_begin, count, sw.al, partial, nullptr, st, nullptr);
       else
-        e = sw.a2 ? launch_mid<V, true, false>(p.T, psi, N, B, gx, a_begin, count, sw.al, partial, nullptr, st)
-                  : launch_mid<V, false, false>(p.T, psi, N, B, gx, a_begin, count, sw.al, partial, nullptr, st);
+        e = sw.a2 ? launch_mid<V, true, false>(p.T, psi, N, B, gx, a_begin, count, sw.al, partial, nullptr, st, nullptr)
+                  : launch_mid<V, false, false>(p.T, psi, N, B, gx, a_begin, count, sw.al, partial, nullptr, st, nullptr);
       if (e != cudaSuccess) return fail(SRE_ECUDA, "launch: %s", cudaGetErrorString(e));
       ra.nslots = gx;
       CK(launch_counted(LK_AUX, st, [&] { k_reduce<<<B, 256, 0, st>>>(partial, ra, sums_dev); return cudaGetLastError(); }));
@@ -395,6 +395,49 @@ int is_device_ptr(const void* ptr, bool& dev) {
     return SRE_OK;
   }
   dev = (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged);
+  return SRE_OK;
+}
+
+// List mode (sre_x_string_sums, N <= 14): one launch per alpha sweep evaluates every X-string of
+// alist_dev (device, n_a <= kListMax); item i's sums land in partial[i] and k_reduce (one block
+// per item, one slot each) writes out_dev row i.  Replaces n_a range calls (5 launches each).
+constexpr int kListMax = 2048;
+
+int run_list(const double2* psi, int N, const uint64_t* alist_dev, int n_a, const double* alpha, int n_alpha,
+             char* ws, double* out_dev, cudaStream_t st) {
+  Dev d;
+  int rc = get_dev(d);
+  if (rc) return rc;
+  Plan p;
+  make_plan(N, d, p, 1);
+  if (!(p.kind == SMALL || p.kind == MID)) return fail(SRE_EINTERNAL, "list mode needs N <= 14");
+  double* partial = reinterpret_cast<double*>(ws);
+  const std::vector<Sweep> sweeps = make_sweeps(alpha, n_alpha);
+  for (const Sweep& sw : sweeps) {
+    ReduceArgs ra;
+    memset(&ra, 0, sizeof(ra));
+    ra.n_alpha = n_alpha;
+    ra.first = sw.first;
+    ra.n_this = sw.al.n;
+    ra.write_common = sw.first == 0;
+    for (int i = 0; i < MAXA; ++i) ra.scale4[i] = sw.scale4[i];
+    ra.err = nullptr;
+    ra.nslots = 1;
+    int gx;
+    cudaError_t e;
+    if (p.kind == SMALL) {
+      const int G = p.T >= 5 ? 32 : (1 << p.T);
+      gx = pick_gx(n_a, 256 / G, 1, occupancy_small(p.T, d));
+      e = sw.a2 ? launch_small<double, true, false>(p.T, psi, N, 1, gx, 0, n_a, sw.al, partial, nullptr, st, alist_dev)
+                : launch_small<double, false, false>(p.T, psi, N, 1, gx, 0, n_a, sw.al, partial, nullptr, st, alist_dev);
+    } else {
+      gx = pick_gx(n_a, 256 >> (p.T - 5), 1, d.sms);
+      e = sw.a2 ? launch_mid<double, true, false>(p.T, psi, N, 1, gx, 0, n_a, sw.al, partial, nullptr, st, alist_dev)
+                : launch_mid<double, false, false>(p.T, psi, N, 1, gx, 0, n_a, sw.al, partial, nullptr, st, alist_dev);
+    }
+    if (e != cudaSuccess) return fail(SRE_ECUDA, "list launch: %s", cudaGetErrorString(e));
+    CK(launch_counted(LK_AUX, st, [&] { k_reduce<<<n_a, 256, 0, st>>>(partial, ra, out_dev); return cudaGetLastError(); }));
+  }
   return SRE_OK;
 }
 
@@ -565,6 +608,27 @@ int sre_x_string_sums(const void* psi, int N, const uint64_t* a_list, int n_a, c
   bool dv = false;
   is_device_ptr(psi, dv);
   if (!dv) return fail(SRE_EINVAL, "psi must be a device pointer");
+  const char* lm = getenv("SRE_LIST");     // SRE_LIST=0: per-X-string ranges (comparison)
+  if (N - 1 <= MID_MAX_T && n_a > 0 && !(lm && lm[0] == '0')) {   // one launch per sweep for the list
+    Dev d;
+    rc = get_dev(d);
+    if (rc) return rc;
+    Plan p;
+    make_plan(N, d, p, 1);
+    const size_t list_off = (size_t)kListMax * NACC * sizeof(double);   // after the item slots
+    if (ws_bytes < list_off + (size_t)kListMax * sizeof(uint64_t) || ws_bytes < ws_bytes_for(p, 1))
+      return fail(SRE_EWORKSPACE, "workspace %zu too small for list mode", ws_bytes);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    uint64_t* dl = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(workspace) + list_off);
+    for (int c0 = 0; c0 < n_a; c0 += kListMax) {
+      const int cn = (n_a - c0) < kListMax ? (n_a - c0) : kListMax;
+      CK(cudaMemcpyAsync(dl, a_list + c0, sizeof(uint64_t) * cn, cudaMemcpyHostToDevice, st));
+      rc = run_list(reinterpret_cast<const double2*>(psi), N, dl, cn, alpha, n_alpha, reinterpret_cast<char*>(workspace),
+                    out_dev + (size_t)c0 * (n_alpha + 2), st);
+      if (rc) return rc;
+    }
+    return SRE_OK;
+  }
   for (int i = 0; i < n_a; ++i) {
     rc = run_range(reinterpret_cast<const double2*>(psi), N, 1, a_list[i], a_list[i] + 1, alpha, n_alpha,
                    reinterpret_cast<char*>(workspace), ws_bytes, out_dev + (size_t)i * (n_alpha + 2),
@@ -643,9 +707,9 @@ int sre_chi(const void* psi, int N, uint64_t a, double* chi_dev, void* stream) {
   al.n = 1;
   cudaError_t e = cudaSuccess;
   if (p.kind == SMALL) {
-    e = launch_small<double, false, true>(p.T, dpsi, N, 1, 1, a, 1, al, nullptr, chi_dev, st);
+    e = launch_small<double, false, true>(p.T, dpsi, N, 1, 1, a, 1, al, nullptr, chi_dev, st, nullptr);
   } else if (p.kind == MID) {
-    e = launch_mid<double, false, true>(p.T, dpsi, N, 1, 1, a, 1, al, nullptr, chi_dev, st);
+    e = launch_mid<double, false, true>(p.T, dpsi, N, 1, 1, a, 1, al, nullptr, chi_dev, st, nullptr);
   } else {
     std::lock_guard<std::mutex> lk(g_cache.mu);
     if (g_cache.dev != d.id) { g_cache.ws = nullptr; g_cache.ws_bytes = 0; g_cache.in = nullptr; g_cache.in_bytes = 0; g_cache.dev = d.id; }

@@ -280,7 +280,10 @@ __device__ __forceinline__ void chi_store(double* chi, uint64_t a, int p, int pl
 // ------------------------------------------------------------------------------------------
 template <int T, bool A2, bool DEBUG, class V = double>
 __global__ void __launch_bounds__(256) k_small(const typename Cx<V>::T* __restrict__ psi_all, int N, uint64_t a0,
-                                               uint64_t count, Alphas al, double* partial, double* chi) {
+                                               uint64_t count, Alphas al, double* partial, double* chi,
+                                               const uint64_t* __restrict__ alist) {
+  // alist != nullptr: list mode (sre_x_string_sums) -- item i is X-string alist[i] and its sums
+  // go to partial[i * NACC] (reduced over its G lanes) instead of the CTA's running slot.
   constexpr int G = T >= 5 ? 32 : (1 << T);
   constexpr int LG = T >= 5 ? 5 : T;
   constexpr int R = (1 << T) / G;
@@ -295,7 +298,7 @@ __global__ void __launch_bounds__(256) k_small(const typename Cx<V>::T* __restri
   for (uint64_t base = warp_first; base < count; base += stride) {
     const uint64_t item = base + ((threadIdx.x & 31) >> LG);
     const bool valid = item < count;
-    const uint64_t a = a0 + item;
+    const uint64_t a = alist ? (valid ? alist[item] : 0) : a0 + item;
     const int p = pivot_of(a, N);
     V A[R], B[R];
 #pragma unroll
@@ -336,8 +339,22 @@ __global__ void __launch_bounds__(256) k_small(const typename Cx<V>::T* __restri
         }
       }
     }
+    if constexpr (!DEBUG) {
+      if (alist) {                     // per-item reduction over the G lanes (all lanes take part)
+#pragma unroll
+        for (int i = 0; i < NACC; ++i) {
+          double x = acc[i];
+#pragma unroll
+          for (int m = 1; m < G; m <<= 1) x += __shfl_xor_sync(0xffffffffu, x, m, G);
+          if (valid && g == 0) partial[(size_t)item * NACC + i] = x;
+          acc[i] = 0.0;
+        }
+      }
+    }
   }
-  if constexpr (!DEBUG) block_flush(acc, partial, blockIdx.y * gridDim.x + blockIdx.x);
+  if constexpr (!DEBUG) {
+    if (!alist) block_flush(acc, partial, blockIdx.y * gridDim.x + blockIdx.x);
+  }
 }
 
 // ------------------------------------------------------------------------------------------
@@ -361,7 +378,9 @@ __device__ __forceinline__ void with_unit_bar(F&& f) {
 
 template <int T, bool A2, bool DEBUG, class V = double>
 __global__ void __launch_bounds__(256, 1) k_mid(const typename Cx<V>::T* __restrict__ psi_all, int N, uint64_t a0,
-                                                uint64_t count, Alphas al, double* partial, double* chi) {
+                                                uint64_t count, Alphas al, double* partial, double* chi,
+                                                const uint64_t* __restrict__ alist) {
+  // alist != nullptr: list mode, as in k_small (per-item sums reduced over the unit).
   constexpr int NT = 1 << (T - 5);
   constexpr int UPC = 256 / NT;
   extern __shared__ double smem[];
@@ -372,8 +391,9 @@ __global__ void __launch_bounds__(256, 1) k_mid(const typename Cx<V>::T* __restr
   double acc[NACC];
 #pragma unroll
   for (int i = 0; i < NACC; ++i) acc[i] = 0.0;
+  __shared__ double lred[8][NACC];   // list mode: per-warp partials of the unit's reduction
   for (uint64_t item = (uint64_t)blockIdx.x * UPC + unit; item < count; item += (uint64_t)gridDim.x * UPC) {
-    const uint64_t a = a0 + item;
+    const uint64_t a = alist ? alist[item] : a0 + item;
     const int p = pivot_of(a, N);
     V v[2][32];
     unit_gen<T, V>(psi, 0, a, p, N, t, v);
@@ -388,9 +408,32 @@ __global__ void __launch_bounds__(256, 1) k_mid(const typename Cx<V>::T* __restr
     } else {
       tile_accumulate<A2>(acc, v[0], al);
       tile_accumulate<A2>(acc, v[1], al);
+      if (alist) {                     // per-item reduction over the unit's NT / 32 warps
+        const int w = threadIdx.x >> 5;
+#pragma unroll
+        for (int i = 0; i < NACC; ++i) {
+          double x = acc[i];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+          if ((threadIdx.x & 31) == 0) lred[w][i] = x;
+          acc[i] = 0.0;
+        }
+        with_unit_bar<T>([&](const auto& bar) { bar.sync(); });
+        if (t == 0) {
+          const int w0 = unit * (NT / 32);
+#pragma unroll
+          for (int i = 0; i < NACC; ++i) {
+            double x = 0.0;
+            for (int k = 0; k < NT / 32; ++k) x += lred[w0 + k][i];
+            partial[(size_t)item * NACC + i] = x;
+          }
+        }
+      }
     }
   }
-  if constexpr (!DEBUG) block_flush(acc, partial, blockIdx.y * gridDim.x + blockIdx.x);
+  if constexpr (!DEBUG) {
+    if (!alist) block_flush(acc, partial, blockIdx.y * gridDim.x + blockIdx.x);
+  }
 }
 
 // ------------------------------------------------------------------------------------------
