@@ -628,7 +628,7 @@ constexpr size_t kSlotBytes = (size_t)kSlots * 2 * sizeof(double);
 void make_mplan(int N, MPlan& m) {
   static const int tab[17][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}, {0, 0, 0},
                                  {0, 0, 0}, {0, 0, 0}, {5, 4, 32}, {6, 4, 32}, {6, 5, 16}, {7, 5, 8},
-                                 {7, 6, 4}, {7, 7, 2}, {8, 7, 4}, {8, 8, 2}};
+                                 {7, 6, 4}, {7, 7, 2}, {7, 8, 2}, {8, 8, 2}};
   m.N = N;
   if (N <= 8) {
     m.single = true;
@@ -698,6 +698,7 @@ ColCFn colc_fn(int H, int S) {
   if (H == 6 && S == 4) return mana::k_mana_colC<6, 4>;
   if (H == 7 && S == 4) return mana::k_mana_colC<7, 4>;
   if (H == 7 && S == 2) return mana::k_mana_colC<7, 2>;
+  if (H == 8 && S == 2) return mana::k_mana_colC<8, 2>;
   return nullptr;
 }
 
