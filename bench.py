@@ -642,6 +642,10 @@ def main():
     roof.update({"kernel": dom, "avg_launch_ms": avg_ms, "launches_timed": prof[dom]["timed"],
                  "share_of_step": share[dom] / tot_ms if world == 1 else None,
                  "ops_per_pauli": ops_unit, "bytes_per_pauli": bytes_unit})
+    if n <= 20:
+        roof["limiter"] = {"resource": "L1TEX data pipe (LDS/STS/SHFL/LDG/STG share it)",
+                           "pct_of_peak": "79-88 (ncu, k_passA10s)",
+                           "source": "profiles/r01_ncu_summary_n20_v3.txt; DESIGN.md section 6"}
     hbm_equiv = 16.0 * value / max(1, world) / 1e9      # FWHT workspace bytes per Pauli string (16 B)
     line = {
         "metric": METRIC, "value": value, "unit": "Pauli strings/s", "n_gpus": world, "steps": args.steps,
