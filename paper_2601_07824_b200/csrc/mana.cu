@@ -571,6 +571,55 @@ __global__ void __launch_bounds__(kThreads) k_mana_colC(ColCArgs A) {
   flush(aa, as, A.slots);
 }
 
+// Pass B with bulk-copy prefetch (H <= 7): each item's contiguous 3^H x S tile arrives by ONE
+// cp.async.bulk (41-93 KB) into a 2-deep ring completed on mbarriers, so the next tile's HBM read
+// overlaps the current tile's transform.  Ragged last column blocks are zero-filled in smem.
+template <int H, int S>
+__global__ void __launch_bounds__(kThreads, 1) k_mana_colT(ColCArgs A) {
+  extern __shared__ __align__(128) double2 ring[];
+  __shared__ __align__(8) uint64_t full[2];
+  constexpr int NH = p3(H);
+  constexpr int E = NH * S;
+  const int NL = p3(A.L);
+  const int nblk = (NL + S - 1) / S;
+  const long items = (long)A.npairs * nblk;
+  if (threadIdx.x == 0) {
+    sre::mbar_init(&full[0], 1);
+    sre::mbar_init(&full[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](long it, int slot) {
+    sre::mbar_expect_tx(&full[slot], E * (unsigned)sizeof(double2));
+    sre::bulk_g2s(ring + (size_t)slot * E, A.ws + (size_t)it * E, E * (unsigned)sizeof(double2), &full[slot]);
+  };
+  if (threadIdx.x == 0)
+    for (int i = 0; i < 2; ++i)
+      if (blockIdx.x + (long)i * gridDim.x < items) issue(blockIdx.x + (long)i * gridDim.x, i);
+  double aa = 0.0, as = 0.0;
+  uint32_t n = 0;
+  for (long it = blockIdx.x; it < items; it += gridDim.x, ++n) {
+    const int slot = (int)(n & 1u);
+    double2* tile = ring + (size_t)slot * E;
+    sre::mbar_wait(&full[slot], (n >> 1) & 1u);
+    const int cb = (int)(it % nblk);
+    const int ncol = min(S, NL - cb * S);
+    if (ncol < S) {                                   // columns pass A never wrote
+      for (int e = threadIdx.x; e < E; e += kThreads)
+        if (e % S >= ncol) tile[e] = make_double2(0.0, 0.0);
+      __syncthreads();
+    }
+    stages<H, S, 0, true>(tile, aa, as);
+    __syncthreads();                                  // everyone is done with this slot
+    if (threadIdx.x == 0) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      const long nx = it + 2L * gridDim.x;
+      if (nx < items) issue(nx, slot);
+    }
+  }
+  flush(aa, as, A.slots);
+}
+
 // Fixed-order sum of the per-CTA slots: out = (S_abs, S_sum).
 __global__ void __launch_bounds__(256) k_mana_reduce(const double* slots, int n, double* out) {
   __shared__ double sa[256], ss[256];
@@ -690,6 +739,17 @@ RowSFn rows_fn(int L, int S) {
   return nullptr;
 }
 
+ColCFn colt_fn(int H, int S) {
+  if (H == 4 && S == 32) return mana::k_mana_colT<4, 32>;
+  if (H == 5 && S == 16) return mana::k_mana_colT<5, 16>;
+  if (H == 5 && S == 8) return mana::k_mana_colT<5, 8>;
+  if (H == 6 && S == 8) return mana::k_mana_colT<6, 8>;
+  if (H == 6 && S == 4) return mana::k_mana_colT<6, 4>;
+  if (H == 7 && S == 4) return mana::k_mana_colT<7, 4>;
+  if (H == 7 && S == 2) return mana::k_mana_colT<7, 2>;
+  return nullptr;
+}
+
 ColCFn colc_fn(int H, int S) {
   if (H == 4 && S == 32) return mana::k_mana_colC<4, 32>;
   if (H == 5 && S == 16) return mana::k_mana_colC<5, 16>;
@@ -789,8 +849,18 @@ int run_mana(const double2* psi, int N, uint64_t a_begin, uint64_t a_end, char* 
       if (P > pairs) P = pairs;
       RowSFn fa = rows_fn(m.L, m.S);
       ColCFn fb = colc_fn(m.H, m.S);
+      size_t smemB = m.col_smem;
+      const char* ct = std::getenv("SRE_MANA_COLT");   // SRE_MANA_COLT=0: plain pass B (comparison)
+      // measured: pass B 803 -> 628 us per launch at N = 14 (H = 7), neutral at H = 6, slower at H = 5
+      if (m.H >= 6 && m.H <= 7 && 2 * m.col_smem <= (size_t)220 * 1024 && !(ct && ct[0] == '0')) {
+        ColCFn ft = colt_fn(m.H, m.S);
+        if (ft) {
+          fb = ft;
+          smemB = 2 * m.col_smem;
+        }
+      }
       if (!fa || !fb) return fail(SRE_EINTERNAL, "no staged mana kernels for N=%d (L=%d H=%d S=%d)", N, m.L, m.H, m.S);
-      const int occA = occupancy((const void*)fa, m.row_smem), occB = occupancy((const void*)fb, m.col_smem);
+      const int occA = occupancy((const void*)fa, m.row_smem), occB = occupancy((const void*)fb, smemB);
       const int nblk = (p3(m.L) + m.S - 1) / m.S;
       for (uint64_t p0 = 0; p0 < pairs; p0 += P) {
         const int np = (int)std::min<uint64_t>(P, pairs - p0);
@@ -800,7 +870,7 @@ int run_mana(const double2* psi, int N, uint64_t a_begin, uint64_t a_end, char* 
         mana::RowSArgs A{psi, rows, a_begin, a_end, p0, np, m.H, m.S, PP};
         mana::ColCArgs B{rows, slots, np, m.L};
         MCK(launch_counted(LK_PASSA, st, [&] { fa<<<gA, kThreads, m.row_smem, st>>>(A); return cudaGetLastError(); }));
-        MCK(launch_counted(LK_PASSB, st, [&] { fb<<<gB, kThreads, m.col_smem, st>>>(B); return cudaGetLastError(); }));
+        MCK(launch_counted(LK_PASSB, st, [&] { fb<<<gB, kThreads, smemB, st>>>(B); return cudaGetLastError(); }));
       }
     } else {
       uint64_t P = (ws_bytes - kSlotBytes) / m.row_bytes;
