@@ -411,10 +411,15 @@ def main_mixed(args):
     import paper_2601_07824_b200 as sre
     from paper_2601_07824_b200 import qutrit
 
+    import torch.distributed as dist
+
     local = int(os.environ.get("LOCAL_RANK", "0"))
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    if world > 1:                                   # replicas: no data-path collective, timing only
+        dist.init_process_group("nccl", device_id=dev)
     label, na, n, depth, seed = MIXED_CONFIGS[args.config]
     d = 3 ** na
     phi = torch.from_numpy(mixed_phi(args.config)).to(dev)
@@ -434,6 +439,9 @@ def main_mixed(args):
         regen()
         m, tr = step()
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
     clocks = Clocks(local)
     launches0 = sre.launch_count()
     sre.profile_begin(1)
@@ -450,8 +458,12 @@ def main_mixed(args):
     launches = sre.launch_count() - launches0
     clk = clocks.stop()
     tot_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
     pts = 9.0 ** na
-    value = args.steps * pts / (tot_ms * 1e-3)
+    value = world * args.steps * pts / (tot_ms * 1e-3)   # every replica processes the whole rho
     # e2e: sre_mana_mixed from pinned host memory (H2D of the whole rho inside the timed region)
     e2e = None
     try:
@@ -460,7 +472,7 @@ def main_mixed(args):
     except Exception:
         avail = 0
     nbytes = d * d * 16
-    if avail > 2.5 * nbytes:
+    if world == 1 and avail > 2.5 * nbytes:
         regen()
         host = torch.empty(d * d, dtype=torch.complex128, pin_memory=True)
         host.copy_(flat)
@@ -476,7 +488,11 @@ def main_mixed(args):
     else:
         e2e = {"value": None, "unit": "phase-space points/s", "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": 16,
                "note": f"host has {avail / 2**30:.0f} GiB available, < 2.5 x {nbytes / 2**30:.0f} GiB needed"}
+    if world > 1:
+        dist.barrier()
     if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
         return 0
     peaks, psrc = load_peaks()
     kinds = {k: v for k, v in prof.items() if v["timed"] > 0 and k != "aux"}
@@ -490,7 +506,7 @@ def main_mixed(args):
             "launches_timed": prof[dom]["timed"], "share_of_step": share[dom] / tot_ms,
             "bytes_per_launch": bytes_launch, "peak_source": psrc}
     line = {
-        "metric": MIXED_METRIC, "value": value, "unit": "phase-space points/s", "n_gpus": 1, "steps": args.steps,
+        "metric": MIXED_METRIC, "value": value, "unit": "phase-space points/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": label, "N_A": na, "N": n, "depth": depth, "seed": seed,
@@ -499,11 +515,13 @@ def main_mixed(args):
         "roofline": roof, "gpu_launches": int(launches), "clocks": clk, "e2e": e2e,
         "result": {"mana": m, "trace": tr}, "profile": prof,
     }
-    if not args.no_cpu_baseline:
+    if world == 1 and not args.no_cpu_baseline:
         import oracle
         oracle.build()
         line["cpu_baseline"] = mixed_oracle_sample()
     print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
     return 0
 
 
