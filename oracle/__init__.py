@@ -175,3 +175,45 @@ def product_state_sums(bloch, alpha: float) -> float:
 def haar_m2(n: int) -> float:
     """Haar-average value M_2^Haar = log2(2^N + 3) - 2. Statistical sanity only."""
     return math.log2(2.0 ** n + 3.0) - 2.0
+
+
+# ---------------------------------------------------------------------------------------------
+# Spectrum epilogue (NEXT-2): histogram of t = |<P>|^2 over all 4^N Pauli strings.
+# ---------------------------------------------------------------------------------------------
+SPECTRUM_BINS = 64
+
+
+def spectrum_bin(t: np.ndarray) -> np.ndarray:
+    """Bin k (0 <= k <= 62) holds round(-log2 t) == k, i.e. t in (2^{-k-1/2}, 2^{-k+1/2}]; bin 63
+    holds everything below 2^{-62.5}, exact zeros included.  The decision uses the float64 value's
+    exponent and a mantissa-vs-sqrt(2) comparison (DESIGN C22)."""
+    t = np.asarray(t, dtype=np.float64)
+    m, e = np.frexp(t)                      # t = m 2^e, m in [0.5, 1)
+    m2 = 2.0 * m                            # t = m2 2^(e-1), m2 in [1, 2)
+    k = -(e - 1) - (m2 > math.sqrt(2.0)).astype(np.int64)   # round(-log2 t)
+    k = np.where(t > 0.0, k, SPECTRUM_BINS - 1)
+    return np.clip(k, 0, SPECTRUM_BINS - 1)
+
+
+def spectrum(psi, a_range=None) -> np.ndarray:
+    """Counts[64] of t = |chi_b(a)|^2 over b in [0, 2^N) and a in a_range (default all), from the
+    oracle's own Alg. 2 chi."""
+    psi = np.asarray(psi, dtype=np.complex128)
+    n = psi.size.bit_length() - 1
+    lo, hi = a_range if a_range is not None else (0, 1 << n)
+    counts = np.zeros(SPECTRUM_BINS, dtype=np.int64)
+    for a in range(lo, hi):
+        c = chi(psi, a)
+        t = (c.real ** 2 + c.imag ** 2)
+        counts += np.bincount(spectrum_bin(t), minlength=SPECTRUM_BINS)
+    return counts
+
+
+def t_state_spectrum(n: int) -> np.ndarray:
+    """|T>^N: per qubit <I,X,Y,Z>^2 = (1, 1/2, 1/2, 0), so t = 2^{-k} with multiplicity
+    C(N,k) 2^k (k qubits carrying X or Y, the rest I) and t = 0 otherwise (4^N - 3^N strings)."""
+    counts = np.zeros(SPECTRUM_BINS, dtype=np.int64)
+    for k in range(n + 1):
+        counts[min(k, SPECTRUM_BINS - 1)] += math.comb(n, k) * 2 ** k
+    counts[SPECTRUM_BINS - 1] += 4 ** n - 3 ** n
+    return counts

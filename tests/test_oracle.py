@@ -175,3 +175,21 @@ def test_haar_concentration(oracle_lib):
     n = 10
     vals = [oracle_lib.sre(si.haar(n, 900 + s), [2.0], "fwht")[0][0] for s in range(4)]
     assert abs(np.mean(vals) - oracle_lib.haar_m2(n)) < 40 * 2.0 ** -n * 4
+
+
+@pytest.mark.parametrize("n", [1, 3, 6])
+def test_spectrum_t_state_closed_form(n):
+    """Spectrum epilogue pin: |T>^N has t = 2^{-k} with multiplicity C(N,k) 2^k, zeros otherwise."""
+    import oracle
+    import sre_inputs as si
+    np.testing.assert_array_equal(oracle.spectrum(si.t_state(n)), oracle.t_state_spectrum(n))
+
+
+def test_spectrum_total_and_bins():
+    import oracle
+    import sre_inputs as si
+    c = oracle.spectrum(si.haar(5, 31))
+    assert c.sum() == 4 ** 5
+    assert c[0] >= 1                       # the identity string: t = 1 -> bin 0
+    b = oracle.spectrum_bin(np.array([1.0, 0.75, 0.70, 0.5, 2.0 ** -10, 0.0, 1e-300]))
+    assert list(b) == [0, 0, 1, 1, 10, 63, 63]
