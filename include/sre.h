@@ -153,6 +153,18 @@ int sre_norm2(const void* psi, int N, int B, double* out_dev, void* stream);
 int sre_chi(const void* psi, int N, uint64_t a, double* chi_dev, void* stream);
 
 /*
+ * sre_pauli_spectrum -- spectrum epilogue (NEXT-2): histogram of t = |<psi|P|psi>|^2 over the
+ * Pauli strings of the X-strings a in [a_begin, a_end) (all 2^N Z-strings of each), from the same
+ * single-pass kernels as the sums (N <= 14).  Bin k (k <= 62) counts round(-log2 t) == k, i.e.
+ * t in (2^{-k-1/2}, 2^{-k+1/2}]; bin 63 counts t < 2^{-62.5} and exact zeros (DESIGN C22).
+ *   hist_dev : device uint64[64], overwritten.   workspace >= sre_workspace_size(N, 1, 1).
+ * Errors: SRE_ERANGE (N > 14 or bad range), SRE_EINVAL, SRE_EWORKSPACE, SRE_ECUDA.  Enqueued on
+ * stream; integer counts, so the result is exact and order-independent.
+ */
+int sre_pauli_spectrum(const void* psi, int N, uint64_t a_begin, uint64_t a_end, uint64_t* hist_dev, void* workspace,
+                       size_t ws_bytes, void* stream);
+
+/*
  * Instrumentation used by bench.py (no effect on results).
  *   sre_launch_count   : cumulative number of kernels this library launched in the process.
  *   sre_profile_begin  : start sampling; every stride-th launch of each kernel kind is bracketed

@@ -62,6 +62,7 @@ def load():
             "sre_exact_ex": ([vp, i, i, dp, i, i, dp, dp], i),
             "sre_partial_sums_ex": ([vp, i, i, u64, u64, dp, i, i, vp, ctypes.c_size_t, vp, vp], i),
             "sre_x_string_sums": ([vp, i, ctypes.POINTER(u64), i, dp, i, vp, ctypes.c_size_t, vp, vp], i),
+            "sre_pauli_spectrum": ([vp, i, u64, u64, vp, vp, ctypes.c_size_t, vp], i),
             "sre_launch_count": ([], u64),
             "sre_profile_begin": ([i], i),
             "sre_profile_end": ([dp, ctypes.POINTER(u64), ctypes.POINTER(u64)], i),
@@ -244,6 +245,30 @@ def chi(psi, a: int):
     torch.cuda.current_stream(psi.device).synchronize()
     del keep
     return torch.view_as_complex(out.view(-1, 2))
+
+
+def spectrum(psi, a_begin: int = 0, a_end: int | None = None, workspace=None, stream=None) -> np.ndarray:
+    """Histogram (numpy int64[64]) of t = |<P>|^2 over the Pauli strings of X-strings
+    [a_begin, a_end) (default all 4^N strings): bin k = round(-log2 t) for k <= 62, bin 63 = t below
+    2^-62.5 or zero (NEXT-2 spectrum epilogue, N <= 14).  psi: cuda complex128 [2^N]."""
+    import torch
+    lib = load()
+    if not (isinstance(psi, torch.Tensor) and psi.is_cuda):
+        raise SreError(1, "spectrum needs a cuda complex128 tensor")
+    ptr, n, b, keep = _psi_ptr(psi)
+    if b != 1:
+        raise SreError(1, "spectrum takes one state")
+    a_end = (1 << n) if a_end is None else a_end
+    hist = torch.empty(64, dtype=torch.int64, device=psi.device)
+    ws_need = workspace_size(n, 1, 1)
+    if workspace is None or workspace.numel() < ws_need:
+        workspace = torch.empty(ws_need, dtype=torch.uint8, device=psi.device)
+    st = stream if stream is not None else torch.cuda.current_stream(psi.device)
+    _check(lib.sre_pauli_spectrum(ctypes.c_void_p(ptr), n, int(a_begin), int(a_end), ctypes.c_void_p(hist.data_ptr()),
+                                  ctypes.c_void_p(workspace.data_ptr()), workspace.numel(),
+                                  ctypes.c_void_p(st.cuda_stream)))
+    del keep
+    return hist.cpu().numpy()
 
 
 KINDS = ("single_pass", "pass_a", "pass_b", "aux", "fused")

@@ -75,19 +75,21 @@ bool tmem_enabled();
 // ------------------------------------------------------------------------------------------
 template <class V, int T, bool A2, bool DBG>
 cudaError_t launch_small_t(const typename Cx<V>::T* psi, int N, int B, int gx, uint64_t a0, uint64_t count, const Alphas& al,
-                           double* partial, double* chi, cudaStream_t st, const uint64_t* alist) {
+                           double* partial, double* chi, cudaStream_t st, const uint64_t* alist,
+                           unsigned long long* hist = nullptr) {
   dim3 grid(gx, B);
   return launch_counted(LK_SINGLE, st, [&] {
-    k_small<T, A2, DBG, V><<<grid, 256, 0, st>>>(psi, N, a0, count, al, partial, chi, alist);
+    k_small<T, A2, DBG, V><<<grid, 256, 0, st>>>(psi, N, a0, count, al, partial, chi, alist, hist);
     return cudaGetLastError();
   });
 }
 
 template <class V, bool A2, bool DBG>
 cudaError_t launch_small(int T, const typename Cx<V>::T* psi, int N, int B, int gx, uint64_t a0, uint64_t count, const Alphas& al,
-                         double* partial, double* chi, cudaStream_t st, const uint64_t* alist) {
+                         double* partial, double* chi, cudaStream_t st, const uint64_t* alist,
+                           unsigned long long* hist = nullptr) {
   switch (T) {
-#define C_(t) case t: return launch_small_t<V, t, A2, DBG>(psi, N, B, gx, a0, count, al, partial, chi, st, alist);
+#define C_(t) case t: return launch_small_t<V, t, A2, DBG>(psi, N, B, gx, a0, count, al, partial, chi, st, alist, hist);
     C_(0) C_(1) C_(2) C_(3) C_(4) C_(5) C_(6) C_(7) C_(8) C_(9) C_(10)
 #undef C_
   }
@@ -103,7 +105,8 @@ cudaError_t set_smem(K kern, int bytes) {
 
 template <class V, int T, bool A2, bool DBG>
 cudaError_t launch_mid_t(const typename Cx<V>::T* psi, int N, int B, int gx, uint64_t a0, uint64_t count, const Alphas& al,
-                         double* partial, double* chi, cudaStream_t st, const uint64_t* alist) {
+                         double* partial, double* chi, cudaStream_t st, const uint64_t* alist,
+                           unsigned long long* hist = nullptr) {
   static bool init = false;
   if (!init) {
     cudaError_t e = set_smem(k_mid<T, A2, DBG, V>, SMEM_128K);
@@ -112,18 +115,19 @@ cudaError_t launch_mid_t(const typename Cx<V>::T* psi, int N, int B, int gx, uin
   }
   dim3 grid(gx, B);
   return launch_counted(LK_SINGLE, st, [&] {
-    k_mid<T, A2, DBG, V><<<grid, 256, SMEM_128K, st>>>(psi, N, a0, count, al, partial, chi, alist);
+    k_mid<T, A2, DBG, V><<<grid, 256, SMEM_128K, st>>>(psi, N, a0, count, al, partial, chi, alist, hist);
     return cudaGetLastError();
   });
 }
 
 template <class V, bool A2, bool DBG>
 cudaError_t launch_mid(int T, const typename Cx<V>::T* psi, int N, int B, int gx, uint64_t a0, uint64_t count, const Alphas& al,
-                       double* partial, double* chi, cudaStream_t st, const uint64_t* alist) {
+                       double* partial, double* chi, cudaStream_t st, const uint64_t* alist,
+                           unsigned long long* hist = nullptr) {
   switch (T) {
-    case 11: return launch_mid_t<V, 11, A2, DBG>(psi, N, B, gx, a0, count, al, partial, chi, st, alist);
-    case 12: return launch_mid_t<V, 12, A2, DBG>(psi, N, B, gx, a0, count, al, partial, chi, st, alist);
-    case 13: return launch_mid_t<V, 13, A2, DBG>(psi, N, B, gx, a0, count, al, partial, chi, st, alist);
+    case 11: return launch_mid_t<V, 11, A2, DBG>(psi, N, B, gx, a0, count, al, partial, chi, st, alist, hist);
+    case 12: return launch_mid_t<V, 12, A2, DBG>(psi, N, B, gx, a0, count, al, partial, chi, st, alist, hist);
+    case 13: return launch_mid_t<V, 13, A2, DBG>(psi, N, B, gx, a0, count, al, partial, chi, st, alist, hist);
   }
   return cudaErrorInvalidValue;
 }
@@ -295,9 +299,9 @@ cudaError_t launch_passBp(const Plan& p, const Dev& d, int kcount, const V* ws, 
 // explicit instantiations: defined in the family translation units
 // ------------------------------------------------------------------------------------------
 #define SRE_SIG_SMALL(V, A2, DBG) cudaError_t launch_small<V, A2, DBG>(int, const typename Cx<V>::T*, int, int, int, \
-    uint64_t, uint64_t, const Alphas&, double*, double*, cudaStream_t, const uint64_t*)
+    uint64_t, uint64_t, const Alphas&, double*, double*, cudaStream_t, const uint64_t*, unsigned long long*)
 #define SRE_SIG_MID(V, A2, DBG) cudaError_t launch_mid<V, A2, DBG>(int, const typename Cx<V>::T*, int, int, int, \
-    uint64_t, uint64_t, const Alphas&, double*, double*, cudaStream_t, const uint64_t*)
+    uint64_t, uint64_t, const Alphas&, double*, double*, cudaStream_t, const uint64_t*, unsigned long long*)
 #define SRE_SIG_PASSA(V) cudaError_t launch_passA<V>(const Plan&, const typename Cx<V>::T*, uint64_t, int, V*, cudaStream_t)
 #define SRE_SIG_PASSB(V, A2, DBG) cudaError_t launch_passB<V, A2, DBG>(const Plan&, uint64_t, int, const V*, \
     const Alphas&, double*, double*, cudaStream_t)

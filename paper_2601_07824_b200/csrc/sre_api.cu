@@ -2,6 +2,7 @@
 // launch schedule and finalisation for the exact SRE hot path (Alg. 2).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -721,6 +722,46 @@ int sre_chi(const void* psi, int N, uint64_t a, double* chi_dev, void* stream) {
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   }
   if (e != cudaSuccess) return fail(SRE_ECUDA, "sre_chi: %s", cudaGetErrorString(e));
+  return SRE_OK;
+}
+
+int sre_pauli_spectrum(const void* psi, int N, uint64_t a_begin, uint64_t a_end, uint64_t* hist_dev, void* workspace,
+                       size_t ws_bytes, void* stream) {
+  g_err[0] = 0;
+  double two = 2.0;
+  int rc = validate_common(psi, N, 1, &two, 1);
+  if (rc) return rc;
+  if (N - 1 > MID_MAX_T) return fail(SRE_ERANGE, "spectrum: N=%d > 14 (single-pass kernels only)", N);
+  if (!hist_dev || !workspace) return fail(SRE_EINVAL, "NULL argument");
+  if (a_begin > a_end || a_end > (1ull << N)) return fail(SRE_ERANGE, "range [%llu, %llu) outside [0, 2^%d]",
+                                                          (unsigned long long)a_begin, (unsigned long long)a_end, N);
+  bool dv = false;
+  is_device_ptr(psi, dv);
+  if (!dv) return fail(SRE_EINVAL, "psi must be a device pointer");
+  Dev d;
+  rc = get_dev(d);
+  if (rc) return rc;
+  Plan p;
+  make_plan(N, d, p, a_end - a_begin);
+  if (ws_bytes < ws_bytes_for(p, 1)) return fail(SRE_EWORKSPACE, "workspace %zu < required %zu", ws_bytes, ws_bytes_for(p, 1));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  unsigned long long* h = reinterpret_cast<unsigned long long*>(hist_dev);
+  CK(cudaMemsetAsync(h, 0, sizeof(unsigned long long) * SPEC_BINS, st));
+  const uint64_t count = a_end - a_begin;
+  if (count == 0) return SRE_OK;
+  const std::vector<Sweep> sw = make_sweeps(&two, 1);
+  const double2* dpsi = reinterpret_cast<const double2*>(psi);
+  double* partial = reinterpret_cast<double*>(workspace);   // the alpha sums are computed and ignored
+  cudaError_t e;
+  if (p.kind == SMALL) {
+    const int G = p.T >= 5 ? 32 : (1 << p.T);
+    const int gx = std::min<int>(pick_gx(count, 256 / G, 1, occupancy_small(p.T, d)), (int)p.slots);
+    e = launch_small<double, true, false>(p.T, dpsi, N, 1, gx, a_begin, count, sw[0].al, partial, nullptr, st, nullptr, h);
+  } else {
+    const int gx = std::min<int>(pick_gx(count, 256 >> (p.T - 5), 1, d.sms), (int)p.slots);
+    e = launch_mid<double, true, false>(p.T, dpsi, N, 1, gx, a_begin, count, sw[0].al, partial, nullptr, st, nullptr, h);
+  }
+  if (e != cudaSuccess) return fail(SRE_ECUDA, "spectrum: %s", cudaGetErrorString(e));
   return SRE_OK;
 }
 

@@ -278,10 +278,35 @@ __device__ __forceinline__ void chi_store(double* chi, uint64_t a, int p, int pl
 // k_small: T = N-1 <= 10.  Group of G = min(32, 2^T) lanes per X-string, R = 2^T/G values
 // per plane per lane; register bits then shuffle bits.  One pass, no workspace.
 // ------------------------------------------------------------------------------------------
+// Spectrum epilogue (NEXT-2, DESIGN C22): bin k = round(-log2 t) for t = |<P>|^2, k <= 62; bin 63
+// holds t < 2^-62.5 and exact zeros.  Decided from the FP64 exponent and mantissa bits.
+constexpr int SPEC_BINS = 64;
+__device__ __forceinline__ int spec_bin(double t) {
+  if (!(t > 0.0)) return SPEC_BINS - 1;
+  const long long b = __double_as_longlong(t);
+  const int e = (int)((b >> 52) & 0x7ff) - 1023;
+  const long long mant = b & 0xfffffffffffffLL;
+  const int k = -e - (mant > 0x6a09e667f3bcdLL ? 1 : 0);   // mantissa of sqrt(2)
+  return k < 0 ? 0 : (k > SPEC_BINS - 1 ? SPEC_BINS - 1 : k);
+}
+template <class V, int M>
+__device__ __forceinline__ void spec_add(unsigned long long* sh, const V (&v)[M]) {
+#pragma unroll
+  for (int j = 0; j < M; ++j) {
+    const double y = (double)v[j];
+    atomicAdd(sh + spec_bin(4.0 * y * y), 1ull);             // t = 4 y^2 (half-length transform)
+  }
+}
+
 template <int T, bool A2, bool DEBUG, class V = double>
 __global__ void __launch_bounds__(256) k_small(const typename Cx<V>::T* __restrict__ psi_all, int N, uint64_t a0,
                                                uint64_t count, Alphas al, double* partial, double* chi,
-                                               const uint64_t* __restrict__ alist) {
+                                               const uint64_t* __restrict__ alist, unsigned long long* hist) {
+  __shared__ unsigned long long shist[SPEC_BINS];   // hist != nullptr: spectrum epilogue
+  if (hist) {
+    for (int i = threadIdx.x; i < SPEC_BINS; i += blockDim.x) shist[i] = 0ull;
+    __syncthreads();
+  }
   // alist != nullptr: list mode (sre_x_string_sums) -- item i is X-string alist[i] and its sums
   // go to partial[i * NACC] (reduced over its G lanes) instead of the CTA's running slot.
   constexpr int G = T >= 5 ? 32 : (1 << T);
@@ -336,6 +361,10 @@ __global__ void __launch_bounds__(256) k_small(const typename Cx<V>::T* __restri
         {
           tile_accumulate<A2>(acc, A, al);
           tile_accumulate<A2>(acc, B, al);
+          if (hist) {
+            spec_add(shist, A);
+            spec_add(shist, B);
+          }
         }
       }
     }
@@ -354,6 +383,11 @@ __global__ void __launch_bounds__(256) k_small(const typename Cx<V>::T* __restri
   }
   if constexpr (!DEBUG) {
     if (!alist) block_flush(acc, partial, blockIdx.y * gridDim.x + blockIdx.x);
+  }
+  if (hist) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < SPEC_BINS; i += blockDim.x)
+      if (shist[i]) atomicAdd(hist + i, shist[i]);
   }
 }
 
@@ -379,7 +413,12 @@ __device__ __forceinline__ void with_unit_bar(F&& f) {
 template <int T, bool A2, bool DEBUG, class V = double>
 __global__ void __launch_bounds__(256, 1) k_mid(const typename Cx<V>::T* __restrict__ psi_all, int N, uint64_t a0,
                                                 uint64_t count, Alphas al, double* partial, double* chi,
-                                                const uint64_t* __restrict__ alist) {
+                                                const uint64_t* __restrict__ alist, unsigned long long* hist) {
+  __shared__ unsigned long long shist[SPEC_BINS];   // hist != nullptr: spectrum epilogue
+  if (hist) {
+    for (int i = threadIdx.x; i < SPEC_BINS; i += blockDim.x) shist[i] = 0ull;
+    __syncthreads();
+  }
   // alist != nullptr: list mode, as in k_small (per-item sums reduced over the unit).
   constexpr int NT = 1 << (T - 5);
   constexpr int UPC = 256 / NT;
@@ -408,6 +447,10 @@ __global__ void __launch_bounds__(256, 1) k_mid(const typename Cx<V>::T* __restr
     } else {
       tile_accumulate<A2>(acc, v[0], al);
       tile_accumulate<A2>(acc, v[1], al);
+      if (hist) {
+        spec_add(shist, v[0]);
+        spec_add(shist, v[1]);
+      }
       if (alist) {                     // per-item reduction over the unit's NT / 32 warps
         const int w = threadIdx.x >> 5;
 #pragma unroll
@@ -433,6 +476,11 @@ __global__ void __launch_bounds__(256, 1) k_mid(const typename Cx<V>::T* __restr
   }
   if constexpr (!DEBUG) {
     if (!alist) block_flush(acc, partial, blockIdx.y * gridDim.x + blockIdx.x);
+  }
+  if (hist) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < SPEC_BINS; i += blockDim.x)
+      if (shist[i]) atomicAdd(hist + i, shist[i]);
   }
 }
 
