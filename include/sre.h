@@ -155,11 +155,13 @@ int sre_chi(const void* psi, int N, uint64_t a, double* chi_dev, void* stream);
 /*
  * sre_pauli_spectrum -- spectrum epilogue (NEXT-2): histogram of t = |<psi|P|psi>|^2 over the
  * Pauli strings of the X-strings a in [a_begin, a_end) (all 2^N Z-strings of each), from the same
- * single-pass kernels as the sums (N <= 14).  Bin k (k <= 62) counts round(-log2 t) == k, i.e.
- * t in (2^{-k-1/2}, 2^{-k+1/2}]; bin 63 counts t < 2^{-62.5} and exact zeros (DESIGN C22).
- *   hist_dev : device uint64[64], overwritten.   workspace >= sre_workspace_size(N, 1, 1).
- * Errors: SRE_ERANGE (N > 14 or bad range), SRE_EINVAL, SRE_EWORKSPACE, SRE_ECUDA.  Enqueued on
- * stream; integer counts, so the result is exact and order-independent.
+ * kernels as the sums (single-pass for N <= 14, pass-B epilogues for N >= 15).  Bin k (k <= 62)
+ * counts round(-log2 t) == k, i.e. t in (2^{-k-1/2}, 2^{-k+1/2}]; bin 63 counts t < 2^{-62.5}
+ * and exact zeros (DESIGN C22).
+ *   hist_dev : device uint64[64], overwritten.
+ *   workspace >= sre_workspace_size(N, 1, 1) + 256 (the tail holds scratch sums for N >= 15).
+ * Errors: SRE_ERANGE (bad range), SRE_EINVAL (also: opt-in SRE_FUSED / SRE_TMEM kernels set),
+ * SRE_EWORKSPACE, SRE_ECUDA.  Enqueued on stream; integer counts, exact and order-independent.
  */
 int sre_pauli_spectrum(const void* psi, int N, uint64_t a_begin, uint64_t a_end, uint64_t* hist_dev, void* workspace,
                        size_t ws_bytes, void* stream);

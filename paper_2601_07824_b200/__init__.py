@@ -250,7 +250,7 @@ def chi(psi, a: int):
 def spectrum(psi, a_begin: int = 0, a_end: int | None = None, workspace=None, stream=None) -> np.ndarray:
     """Histogram (numpy int64[64]) of t = |<P>|^2 over the Pauli strings of X-strings
     [a_begin, a_end) (default all 4^N strings): bin k = round(-log2 t) for k <= 62, bin 63 = t below
-    2^-62.5 or zero (NEXT-2 spectrum epilogue, N <= 14).  psi: cuda complex128 [2^N]."""
+    2^-62.5 or zero (NEXT-2 spectrum epilogue, any N).  psi: cuda complex128 [2^N]."""
     import torch
     lib = load()
     if not (isinstance(psi, torch.Tensor) and psi.is_cuda):
@@ -260,7 +260,7 @@ def spectrum(psi, a_begin: int = 0, a_end: int | None = None, workspace=None, st
         raise SreError(1, "spectrum takes one state")
     a_end = (1 << n) if a_end is None else a_end
     hist = torch.empty(64, dtype=torch.int64, device=psi.device)
-    ws_need = workspace_size(n, 1, 1)
+    ws_need = workspace_size(n, 1, 1) + 256
     if workspace is None or workspace.numel() < ws_need:
         workspace = torch.empty(ws_need, dtype=torch.uint8, device=psi.device)
     st = stream if stream is not None else torch.cuda.current_stream(psi.device)

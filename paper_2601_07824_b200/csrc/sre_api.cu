@@ -255,7 +255,8 @@ int occupancy_small(int T, const Dev& d) {
 // V = double: FP64 path; V = float: FP32 mode (psi already converted to complex64)
 template <class V>
 int run_range_t(const typename Cx<V>::T* psi, const Plan& p, const Dev& d, int N, int B, uint64_t a_begin,
-                uint64_t a_end, const double* alpha, int n_alpha, char* ws, double* sums_dev, cudaStream_t st) {
+                uint64_t a_end, const double* alpha, int n_alpha, char* ws, double* sums_dev, cudaStream_t st,
+                unsigned long long* hist = nullptr) {
   constexpr bool F64 = std::is_same<V, double>::value;
   double* partial = reinterpret_cast<double*>(ws);
   V* slab = reinterpret_cast<V*>(ws + off_slab(p, B));
@@ -266,6 +267,8 @@ int run_range_t(const typename Cx<V>::T* psi, const Plan& p, const Dev& d, int N
   if (count == 0) return SRE_OK;
   const std::vector<Sweep> sweeps = make_sweeps(alpha, n_alpha);
   for (const Sweep& sw : sweeps) {
+    Alphas al_h = sw.al;   // spectrum epilogue pointer rides in the alphas (two-pass kernels)
+    al_h.hist = hist;
     ReduceArgs ra;
     memset(&ra, 0, sizeof(ra));
     ra.n_alpha = n_alpha;
@@ -286,11 +289,11 @@ int run_range_t(const typename Cx<V>::T* psi, const Plan& p, const Dev& d, int N
       CK(cudaMemsetAsync(partial, 0, sizeof(double) * (size_t)gx * B * NACC, st));
       cudaError_t e;
       if (p.kind == SMALL)
-        e = sw.a2 ? launch_small<V, true, false>(p.T, psi, N, B, gx, a_begin, count, sw.al, partial, nullptr, st, nullptr)
-                  : launch_small<V, false, false>(p.T, psi, N, B, gx, a_begin, count, sw.al, partial, nullptr, st, nullptr);
+        e = sw.a2 ? launch_small<V, true, false>(p.T, psi, N, B, gx, a_begin, count, al_h, partial, nullptr, st, nullptr)
+                  : launch_small<V, false, false>(p.T, psi, N, B, gx, a_begin, count, al_h, partial, nullptr, st, nullptr);
       else
-        e = sw.a2 ? launch_mid<V, true, false>(p.T, psi, N, B, gx, a_begin, count, sw.al, partial, nullptr, st, nullptr)
-                  : launch_mid<V, false, false>(p.T, psi, N, B, gx, a_begin, count, sw.al, partial, nullptr, st, nullptr);
+        e = sw.a2 ? launch_mid<V, true, false>(p.T, psi, N, B, gx, a_begin, count, al_h, partial, nullptr, st, nullptr)
+                  : launch_mid<V, false, false>(p.T, psi, N, B, gx, a_begin, count, al_h, partial, nullptr, st, nullptr);
       if (e != cudaSuccess) return fail(SRE_ECUDA, "launch: %s", cudaGetErrorString(e));
       ra.nslots = gx;
       CK(launch_counted(LK_AUX, st, [&] { k_reduce<<<B, 256, 0, st>>>(partial, ra, sums_dev); return cudaGetLastError(); }));
@@ -304,8 +307,8 @@ int run_range_t(const typename Cx<V>::T* psi, const Plan& p, const Dev& d, int N
             const int kc = (int)((hi - a) < (uint64_t)p.K ? (hi - a) : (uint64_t)p.K);
             cudaError_t e = launch_passA<V>(p, ps, a, kc, slab, st);
             if (e != cudaSuccess) return fail(SRE_ECUDA, "passA: %s", cudaGetErrorString(e));
-            e = sw.a2 ? launch_passB<V, true, false>(p, a, kc, slab, sw.al, partial, nullptr, st)
-                      : launch_passB<V, false, false>(p, a, kc, slab, sw.al, partial, nullptr, st);
+            e = sw.a2 ? launch_passB<V, true, false>(p, a, kc, slab, al_h, partial, nullptr, st)
+                      : launch_passB<V, false, false>(p, a, kc, slab, al_h, partial, nullptr, st);
             if (e != cudaSuccess) return fail(SRE_ECUDA, "passB: %s", cudaGetErrorString(e));
           }
           return SRE_OK;
@@ -323,15 +326,15 @@ int run_range_t(const typename Cx<V>::T* psi, const Plan& p, const Dev& d, int N
           const uint64_t per = (uint64_t)8 * p.KG;
           if constexpr (F64) {   // FP64-only experimental paths
             if (fused_enabled() && p.L == 10 && s0 < a_end) {   // one persistent launch for the aligned bulk
-              cudaError_t e = sw.a2 ? launch_fused<true>(p, d, ps, s0, a_end - s0, slab, ctl, sw.al, partial, st)
-                                    : launch_fused<false>(p, d, ps, s0, a_end - s0, slab, ctl, sw.al, partial, st);
+              cudaError_t e = sw.a2 ? launch_fused<true>(p, d, ps, s0, a_end - s0, slab, ctl, al_h, partial, st)
+                                    : launch_fused<false>(p, d, ps, s0, a_end - s0, slab, ctl, al_h, partial, st);
               if (e != cudaSuccess) return fail(SRE_ECUDA, "fused: %s", cudaGetErrorString(e));
               s0 = a_end;
             }
             if (p.tmem) {
               for (uint64_t a = s0; a < a_end; a += per) {
                 const int kc = (int)((a_end - a) < per ? (a_end - a) : per);
-                cudaError_t e = launch_tmem_pair(p, d, sw.a2, ps, a, kc, slab, sw.al, partial, st);
+                cudaError_t e = launch_tmem_pair(p, d, sw.a2, ps, a, kc, slab, al_h, partial, st);
                 if (e != cudaSuccess) return fail(SRE_ECUDA, "tmem pair: %s", cudaGetErrorString(e));
               }
               s0 = a_end;
@@ -341,8 +344,8 @@ int run_range_t(const typename Cx<V>::T* psi, const Plan& p, const Dev& d, int N
             const int kc = (int)((a_end - a) < per ? (a_end - a) : per);
             cudaError_t e = launch_passA10s<V>(p, d, ps, a, kc, slab, st);
             if (e != cudaSuccess) return fail(SRE_ECUDA, "passA10s: %s", cudaGetErrorString(e));
-            e = sw.a2 ? launch_passBp<V, true>(p, d, kc, slab, sw.al, partial, st)
-                      : launch_passBp<V, false>(p, d, kc, slab, sw.al, partial, st);
+            e = sw.a2 ? launch_passBp<V, true>(p, d, kc, slab, al_h, partial, st)
+                      : launch_passBp<V, false>(p, d, kc, slab, al_h, partial, st);
             if (e != cudaSuccess) return fail(SRE_ECUDA, "passBp: %s", cudaGetErrorString(e));
           }
         }
@@ -358,7 +361,8 @@ int run_range_t(const typename Cx<V>::T* psi, const Plan& p, const Dev& d, int N
 }
 
 int run_range(const double2* psi, int N, int B, uint64_t a_begin, uint64_t a_end, const double* alpha, int n_alpha,
-              char* ws, size_t ws_bytes, double* sums_dev, cudaStream_t st, int prec = SRE_FP64) {
+              char* ws, size_t ws_bytes, double* sums_dev, cudaStream_t st, int prec = SRE_FP64,
+              unsigned long long* hist = nullptr) {
   Dev d;
   int rc = get_dev(d);
   if (rc) return rc;
@@ -372,7 +376,7 @@ int run_range(const double2* psi, int N, int B, uint64_t a_begin, uint64_t a_end
     CK(launch_counted(LK_AUX, st, [&] { k_to_f32<<<4 * d.sms, 256, 0, st>>>(psi, p32, n); return cudaGetLastError(); }));
     return run_range_t<float>(p32, p, d, N, B, a_begin, a_end, alpha, n_alpha, ws, sums_dev, st);
   }
-  return run_range_t<double>(psi, p, d, N, B, a_begin, a_end, alpha, n_alpha, ws, sums_dev, st);
+  return run_range_t<double>(psi, p, d, N, B, a_begin, a_end, alpha, n_alpha, ws, sums_dev, st, hist);
 }
 
 int validate_common(const void* psi, int N, int B, const double* alpha, int n_alpha) {
@@ -731,7 +735,6 @@ int sre_pauli_spectrum(const void* psi, int N, uint64_t a_begin, uint64_t a_end,
   double two = 2.0;
   int rc = validate_common(psi, N, 1, &two, 1);
   if (rc) return rc;
-  if (N - 1 > MID_MAX_T) return fail(SRE_ERANGE, "spectrum: N=%d > 14 (single-pass kernels only)", N);
   if (!hist_dev || !workspace) return fail(SRE_EINVAL, "NULL argument");
   if (a_begin > a_end || a_end > (1ull << N)) return fail(SRE_ERANGE, "range [%llu, %llu) outside [0, 2^%d]",
                                                           (unsigned long long)a_begin, (unsigned long long)a_end, N);
@@ -749,6 +752,14 @@ int sre_pauli_spectrum(const void* psi, int N, uint64_t a_begin, uint64_t a_end,
   CK(cudaMemsetAsync(h, 0, sizeof(unsigned long long) * SPEC_BINS, st));
   const uint64_t count = a_end - a_begin;
   if (count == 0) return SRE_OK;
+  if (p.kind == TWOPASS) {   // pass-B epilogues bin the final values; sums go to a scratch tail
+    if (fused_enabled() || p.tmem) return fail(SRE_EINVAL, "spectrum needs the default kernels (unset SRE_FUSED/SRE_TMEM)");
+    const size_t need = ws_bytes_for(p, 1) + 256;
+    if (ws_bytes < need) return fail(SRE_EWORKSPACE, "workspace %zu < required %zu", ws_bytes, need);
+    double* scratch = reinterpret_cast<double*>(reinterpret_cast<char*>(workspace) + ws_bytes_for(p, 1));
+    return run_range(reinterpret_cast<const double2*>(psi), N, 1, a_begin, a_end, &two, 1,
+                     reinterpret_cast<char*>(workspace), ws_bytes_for(p, 1), scratch, st, SRE_FP64, h);
+  }
   const std::vector<Sweep> sw = make_sweeps(&two, 1);
   const double2* dpsi = reinterpret_cast<const double2*>(psi);
   double* partial = reinterpret_cast<double*>(workspace);   // the alpha sums are computed and ignored

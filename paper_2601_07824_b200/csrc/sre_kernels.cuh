@@ -33,6 +33,7 @@ struct Alphas {
   int n;                // alphas in this sweep
   int need_log;         // any alpha == 1
   int any_real;         // any kind == 2 (non-integer alpha)
+  unsigned long long* hist;   // spectrum epilogue (two-pass kernels; nullptr = off)
   int kind[MAXA];       // 0: integer exponent iexp[i] >= 1, 2: general real power
   int iexp[MAXA];
   double alpha[MAXA];
@@ -532,6 +533,11 @@ template <int TP, int CB, bool A2, bool DEBUG, class V = double>
 __global__ void __launch_bounds__(TP >= 14 ? 512 : 256, 1) k_passB(int N, int L, uint64_t a0, int kcount,
                                                                    const V* __restrict__ ws, Alphas al,
                                                                    double* partial, double* chi) {
+  __shared__ unsigned long long shist[SPEC_BINS];
+  if (al.hist) {
+    for (int i = threadIdx.x; i < SPEC_BINS; i += blockDim.x) shist[i] = 0ull;
+    __syncthreads();
+  }
   constexpr int NT = 1 << (TP - 5);
   constexpr int BLK = TP >= 14 ? 512 : 256;
   constexpr int UPC = BLK / NT;
@@ -572,10 +578,18 @@ __global__ void __launch_bounds__(TP >= 14 ? 512 : 256, 1) k_passB(int N, int L,
       }
     } else {
       tile_accumulate<A2>(acc, v[0], al);
+      if constexpr (!DEBUG && std::is_same<V, double>::value) {
+        if (al.hist) spec_add(shist, v[0]);
+      }
     }
   }
   (void)H;
   if constexpr (!DEBUG) block_flush(acc, partial, blockIdx.x);
+  if (al.hist) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < SPEC_BINS; i += blockDim.x)
+      if (shist[i]) atomicAdd(al.hist + i, shist[i]);
+  }
 }
 
 // ------------------------------------------------------------------------------------------
@@ -761,6 +775,11 @@ __global__ void __launch_bounds__(256, 1) k_passBt(int N, int kcount, const V* _
   if (t == 0)
     for (int i = 0; i < PBT_NS; ++i)
       if (first + i * step < tiles) issue(first + i * step, i);
+  __shared__ unsigned long long shist[SPEC_BINS];   // al.hist: spectrum epilogue
+  if (al.hist) {
+    for (int i = threadIdx.x; i < SPEC_BINS; i += blockDim.x) shist[i] = 0ull;
+    __syncthreads();
+  }
   double acc[NACC];
 #pragma unroll
   for (int i = 0; i < NACC; ++i) acc[i] = 0.0;
@@ -780,8 +799,16 @@ __global__ void __launch_bounds__(256, 1) k_passBt(int N, int kcount, const V* _
       if (nx < tiles) issue(nx, slot);
     }
     tile_accumulate<A2>(acc, v[0], al);
+    if constexpr (std::is_same<V, double>::value) {
+      if (al.hist) spec_add(shist, v[0]);
+    }
   }
   block_flush(acc, partial, blockIdx.x);
+  if (al.hist) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < SPEC_BINS; i += blockDim.x)
+      if (shist[i]) atomicAdd(al.hist + i, shist[i]);
+  }
 }
 
 // ------------------------------------------------------------------------------------------

@@ -50,5 +50,22 @@ def test_ranges_and_errors(sre):
     np.testing.assert_array_equal(sre.spectrum(psi, 0, k) + sre.spectrum(psi, k, 1 << 12), whole)
     assert sre.spectrum(psi, 5, 5).sum() == 0
     with pytest.raises(SreError) as e:
-        sre.spectrum(_cuda(si.haar(15, 1)))
+        sre.spectrum(psi, 10, 5000)
     assert e.value.code == 2
+
+
+@pytest.mark.parametrize("n", [15, 16, 21])
+def test_t_state_two_pass(sre, n):
+    """Pass-B epilogues (staged N = 15-20, streamed N = 21-25, generic heads a < 1024)."""
+    import oracle
+    import sre_inputs as si
+    np.testing.assert_array_equal(sre.spectrum(_cuda(si.t_state(n))), oracle.t_state_spectrum(n))
+
+
+@pytest.mark.parametrize("lo,hi", [(0, 24), (2048, 2080), (1021, 1043)])
+def test_two_pass_vs_oracle(sre, lo, hi):
+    """N = 16 brick-wall: generic heads, aligned staged groups and a range straddling both."""
+    import oracle
+    import sre_inputs as si
+    psi = si.brickwall(16, 3, 1500)
+    np.testing.assert_array_equal(sre.spectrum(_cuda(psi), lo, hi), oracle.spectrum(psi, (lo, hi)))
