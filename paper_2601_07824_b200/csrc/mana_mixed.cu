@@ -112,7 +112,7 @@ __device__ __forceinline__ void leg_stage(double2* tile, double2* g, long base, 
     for (int r = 0; r < 3; ++r)
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        if constexpr (LDG) x[r][c] = __ldcs(g + gb + r * gr + c * gc);
+        if constexpr (LDG) x[r][c] = __ldg(g + gb + r * gr + c * gc);
         else x[r][c] = tile[tb + r * sr + c * sc];
       }
     leg9(x);
