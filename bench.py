@@ -54,6 +54,17 @@ MIXED_METRIC = "exact mixed-state qutrit mana, phase-space points/s (9^N_A per d
 FP64_OPS_PER_CLK_SM = 64        # B200 FP64 pipe (measured 63.9/clk/SM, profiles/r01_microbench.json)
 
 
+def ncu_traffic(config, kind):
+    """roofline.traffic: DRAM bytes per launch of the dominant kernel from the committed `ncu --set full`
+    capture of this config (profiles/r01_traffic.json, written by tools/ncu_traffic.py), else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+            t = json.load(f).get(config)
+    except (OSError, ValueError):
+        return None
+    return t["dram_bytes_per_launch"] if t and t.get("kind") == kind else None
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -326,7 +337,7 @@ def main_mana(args):
     peak = FP64_OPS_PER_CLK_SM * 148 * sm_mhz * 1e6 / 1e12
     achieved = ops_pt * pts_per_launch / (avg_ms * 1e-3) / 1e12
     roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s (FP64 ops)", "frac": achieved / peak,
-            "traffic": None, "kernel": dom, "avg_launch_ms": avg_ms, "launches_timed": prof[dom]["timed"],
+            "traffic": ncu_traffic(args.config, dom), "kernel": dom, "avg_launch_ms": avg_ms, "launches_timed": prof[dom]["timed"],
             "share_of_step": share[dom] / tot_ms if world == 1 else None, "ops_per_point": ops_pt,
             "peak_source": f"64 FP64 ops/clk/SM x 148 SMs x {sm_mhz:.0f} MHz",
             "note": "measured limiter is the L1TEX/shared-memory data pipe (profiles/r01_ncu_summary_mana14.txt)"}
@@ -502,7 +513,7 @@ def main_mixed(args):
     bytes_launch = (2.0 if dom == "pass_a" else 1.0) * nbytes    # non-final pass: read + write; final: read
     achieved = bytes_launch / (avg_ms * 1e-3) / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-            "frac": achieved / peaks["hbm_gbs"], "traffic": None, "kernel": dom, "avg_launch_ms": avg_ms,
+            "frac": achieved / peaks["hbm_gbs"], "traffic": ncu_traffic(args.config, dom), "kernel": dom, "avg_launch_ms": avg_ms,
             "launches_timed": prof[dom]["timed"], "share_of_step": share[dom] / tot_ms,
             "bytes_per_launch": bytes_launch, "peak_source": psrc}
     line = {
@@ -657,6 +668,7 @@ def main():
         roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s (FP64 ops)",
                 "frac": achieved / peak, "traffic": None,
                 "peak_source": f"64 FP64 ops/clk/SM x 148 SMs x {sm_mhz:.0f} MHz (guide unit count; measured 63.9)"}
+    roof["traffic"] = ncu_traffic(args.config, dom)
     roof.update({"kernel": dom, "avg_launch_ms": avg_ms, "launches_timed": prof[dom]["timed"],
                  "share_of_step": share[dom] / tot_ms if world == 1 else None,
                  "ops_per_pauli": ops_unit, "bytes_per_pauli": bytes_unit})
