@@ -14,9 +14,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsre_b200.so")
-UNITS = ["sre_api.cu", "k_small.cu", "k_mid.cu", "k_generic.cu", "k_stageA.cu", "k_stageB.cu", "k_exp.cu", "mana.cu", "mana_mixed.cu"]
+UNITS = ["sre_api.cu", "k_small.cu", "k_mid.cu", "k_generic.cu", "k_stageA.cu", "k_stageB.cu", "mana.cu", "mana_mixed.cu"]
 SOURCES = [os.path.join(CSRC, u) for u in UNITS]
-HEADERS = [os.path.join(CSRC, h) for h in ("sre_kernels.cuh", "tmem.cuh", "launch.cuh")] + \
+HEADERS = [os.path.join(CSRC, h) for h in ("sre_kernels.cuh", "launch.cuh")] + \
     [os.path.join(ROOT, "include", "sre.h")]
 DEPS = SOURCES + HEADERS
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -62,13 +62,12 @@ struct Plan {
   int unitsA = 0, unitsB = 0, blkB = 0;
   size_t slab_doubles = 0;  // K * 2^N
   size_t slots = 0;         // partial slots per state
-  bool staged = false;      // L == 10: k_passA10s + k_passBp
-  bool tmem = false;        // N = 19, 20: TMEM pass B (H = 8) + k_passA11t / k_passA10s<RM>
-  uint64_t amin = 0;        // first X-string the staged / TMEM kernels accept (a_h != 0)
-  int KG = 0;               // 8-X-string groups per staged launch
+  bool staged = false;      // staged (N = 15..20) or streamed (N = 21..25) pass A + TMA-fed pass B
+  uint64_t amin = 0;        // first X-string the staged / streamed kernels accept (a_h != 0)
+  int KG = 0;               // 8-X-string groups per staged / streamed launch pair
+  bool legacyA = false;     // SRE_LEGACY_A=1: round-1 three-round k_passAs for N = 21..24 (comparison)
+  bool legacyB = false;     // SRE_LEGACY_B=1: round-1 three-round k_passBt<13, CB> for N = 21..24 (comparison)
 };
-
-bool tmem_enabled();
 
 // ------------------------------------------------------------------------------------------
 // launchers (template dispatch)
@@ -195,7 +194,7 @@ cudaError_t launch_passA10s_t(const Dev& d, const typename Cx<V>::T* psi, uint64
                               cudaStream_t st) {
   static bool init = false;
   if (!init) {
-    cudaError_t e = set_smem(k_passA10s<N, false, V>, PA10_SMEM);
+    cudaError_t e = set_smem(k_passA10s<N, V>, PA10_SMEM);
     if (e != cudaSuccess) return e;
     init = true;
   }
@@ -203,13 +202,10 @@ cudaError_t launch_passA10s_t(const Dev& d, const typename Cx<V>::T* psi, uint64
   const uint64_t items = (uint64_t)groups << (N - 11);
   const unsigned grid = (unsigned)(items < (uint64_t)d.sms ? items : (uint64_t)d.sms);
   return launch_counted(LK_PASSA, st, [&] {
-    k_passA10s<N, false, V><<<grid, 256, PA10_SMEM, st>>>(psi, a_first, kcount, groups, ws);
+    k_passA10s<N, V><<<grid, 256, PA10_SMEM, st>>>(psi, a_first, kcount, groups, ws);
     return cudaGetLastError();
   });
 }
-
-cudaError_t launch_tmem_pair(const Plan& p, const Dev& d, bool a2, const double2* psi, uint64_t a_first, int kcount,
-                             double* ws, const Alphas& al, double* partial, cudaStream_t st);
 
 template <class V, int N, int L>
 cudaError_t launch_passAs_t(const Dev& d, const typename Cx<V>::T* psi, uint64_t a_first, int kcount, V* ws,
@@ -229,9 +225,35 @@ cudaError_t launch_passAs_t(const Dev& d, const typename Cx<V>::T* psi, uint64_t
   });
 }
 
+template <int N>
+cudaError_t launch_passAr_t(const Dev& d, const double2* psi, uint64_t a_first, int kcount, double* ws, cudaStream_t st) {
+  static bool init = false;
+  if (!init) {
+    cudaError_t e = set_smem(k_passAq<N>, PAQ_SMEM);
+    if (e != cudaSuccess) return e;
+    init = true;
+  }
+  const uint64_t items = (uint64_t)kcount << (N - 15);               // (4-row block, X-string)
+  const unsigned grid = (unsigned)(items < (uint64_t)d.sms ? items : (uint64_t)d.sms);
+  return launch_counted(LK_PASSA, st, [&] {
+    k_passAq<N><<<grid, 256, PAQ_SMEM, st>>>(psi, a_first, kcount, ws);
+    return cudaGetLastError();
+  });
+}
+
 template <class V>
 cudaError_t launch_passA10s(const Plan& p, const Dev& d, const typename Cx<V>::T* psi, uint64_t a_first, int kcount,
                             V* ws, cudaStream_t st) {
+  if constexpr (std::is_same<V, double>::value) {   // FP64 N = 21..24: radix-64 pass A (TMEM-parked plane B)
+    if (p.N >= 21 && p.N <= 24 && !p.legacyA) {
+      switch (p.N) {
+        case 21: return launch_passAr_t<21>(d, psi, a_first, kcount, ws, st);
+        case 22: return launch_passAr_t<22>(d, psi, a_first, kcount, ws, st);
+        case 23: return launch_passAr_t<23>(d, psi, a_first, kcount, ws, st);
+        case 24: return launch_passAr_t<24>(d, psi, a_first, kcount, ws, st);
+      }
+    }
+  }
   switch (p.N) {
     case 21: return launch_passAs_t<V, 21, 12>(d, psi, a_first, kcount, ws, st);
     case 22: return launch_passAs_t<V, 22, 12>(d, psi, a_first, kcount, ws, st);
@@ -247,11 +269,6 @@ cudaError_t launch_passA10s(const Plan& p, const Dev& d, const typename Cx<V>::T
   }
   return cudaErrorInvalidValue;
 }
-
-bool fused_enabled();
-template <bool A2>
-cudaError_t launch_fused(const Plan& p, const Dev& d, const double2* psi, uint64_t a_first, uint64_t count,
-                         double* ws, FusedCtl* ctl, const Alphas& al, double* partial, cudaStream_t st);
 
 template <class V, int TP, int CB, bool A2>
 cudaError_t launch_passBt_t(const Plan& p, const Dev& d, int kcount, const V* ws, const Alphas& al,
@@ -269,9 +286,34 @@ cudaError_t launch_passBt_t(const Plan& p, const Dev& d, int kcount, const V* ws
   });
 }
 
+template <int CB, bool A2>
+cudaError_t launch_passBr_t(const Dev& d, int kcount, const double* ws, const Alphas& al, double* partial,
+                            cudaStream_t st) {
+  static bool init = false;
+  if (!init) {
+    cudaError_t e = set_smem(k_passBr<CB, A2>, PBR_SMEM);
+    if (e != cudaSuccess) return e;
+    init = true;
+  }
+  return launch_counted(LK_PASSB, st, [&] {
+    k_passBr<CB, A2><<<d.sms, 256, PBR_SMEM, st>>>(kcount, ws, al, partial);
+    return cudaGetLastError();
+  });
+}
+
 template <class V, bool A2>
 cudaError_t launch_passBp(const Plan& p, const Dev& d, int kcount, const V* ws, const Alphas& al, double* partial,
                           cudaStream_t st) {
+  if constexpr (std::is_same<V, double>::value) {   // FP64 N = 21..24: radix-64 pass B (one transpose)
+    if (p.N >= 21 && p.N <= 24 && !p.legacyB) {
+      switch (13 - p.H) {
+        case 5: return launch_passBr_t<5, A2>(d, kcount, ws, al, partial, st);
+        case 4: return launch_passBr_t<4, A2>(d, kcount, ws, al, partial, st);
+        case 3: return launch_passBr_t<3, A2>(d, kcount, ws, al, partial, st);
+        case 2: return launch_passBr_t<2, A2>(d, kcount, ws, al, partial, st);
+      }
+    }
+  }
   if (p.N >= 21) {     // streamed path: tiles of 2^13 doubles, CB = 13 - H
     switch (13 - p.H) {
       case 7: return launch_passBt_t<V, 13, 7, A2>(p, d, kcount, ws, al, partial, st);
@@ -309,8 +351,6 @@ cudaError_t launch_passBp(const Plan& p, const Dev& d, int kcount, const V* ws, 
     int, V*, cudaStream_t)
 #define SRE_SIG_STAGEB(V, A2) cudaError_t launch_passBp<V, A2>(const Plan&, const Dev&, int, const V*, const Alphas&, \
     double*, cudaStream_t)
-#define SRE_SIG_FUSED(A2) cudaError_t launch_fused<A2>(const Plan&, const Dev&, const double2*, uint64_t, uint64_t, \
-    double*, FusedCtl*, const Alphas&, double*, cudaStream_t)
 #define SRE_FOR_V_A2_DBG(M, P) P M(double, true, false); P M(double, false, false); P M(float, true, false); \
     P M(float, false, false); P M(double, false, true)
 #define SRE_FOR_V(M, P) P M(double); P M(float)
@@ -331,10 +371,6 @@ SRE_FOR_V(SRE_SIG_STAGEA, extern template);
 #endif
 #ifndef SRE_FAMILY_STAGEB
 SRE_FOR_V_A2(SRE_SIG_STAGEB, extern template);
-#endif
-#ifndef SRE_FAMILY_EXP
-extern template SRE_SIG_FUSED(true);
-extern template SRE_SIG_FUSED(false);
 #endif
 
 }  // namespace sre_host

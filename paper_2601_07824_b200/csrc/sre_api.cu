@@ -81,11 +81,6 @@ int get_dev(Dev& d) {
 // ------------------------------------------------------------------------------------------
 // plan
 // ------------------------------------------------------------------------------------------
-bool tmem_enabled() {  // opt-in (SRE_TMEM=1): the 4-warp TMEM pass B measured slower (37 vs 30 us)
-  const char* e = getenv("SRE_TMEM");
-  return e && e[0] == '1';
-}
-
 int staged_groups(int N) {
   const char* e = getenv("SRE_KG");
   if (e && atoi(e) > 0) return atoi(e) > 1024 ? 1024 : atoi(e);
@@ -151,19 +146,27 @@ int make_plan(int N, const Dev& d, Plan& p, uint64_t count = ~0ull) {
     p.slab_doubles = (size_t)p.K << N;
     const uint64_t itemsB = (uint64_t)p.K * 2 * (1ull << (p.L - p.CB));
     p.slots = (size_t)((itemsB + p.unitsB - 1) / p.unitsB);
-    if (N >= 21 && N <= 25) {  // streamed pass A (k_passAs) + TMA-fed pass B with 2^13-double tiles
+    if (N >= 21 && N <= 25) {  // streamed pass A (k_passAr / k_passAs) + TMA-fed pass B with 2^13-double tiles
+      // X-strings per launch pair: the launch's groups read each psi row pair from L2 after its first
+      // HBM fetch, so psi traffic per X-string is 2^(N+4) / K bytes (N = 24, K = 32: 8 MiB vs a
+      // 128 MiB workspace round trip); workspace K x 2^(N+3) bytes (N = 24: 4 GiB)
+      int kk = N == 21 ? 64 : 32;
       if (const char* e = getenv("SRE_K")) {   // experiments: X-strings per streamed launch pair
-        const int kk = atoi(e);
-        if (kk >= 8 && kk <= 512) {
-          p.K = kk;
-          p.slab_doubles = (size_t)p.K << N;
-          p.slots = (size_t)(((uint64_t)p.K * 2 * (1ull << (p.L - p.CB)) + p.unitsB - 1) / p.unitsB);
-        }
+        const int ke = atoi(e);
+        if (ke >= 8 && ke <= 512) kk = ke & ~7;
       }
+      if ((uint64_t)kk > count) kk = (int)(((count + 7) / 8) * 8 > 0 ? ((count + 7) / 8) * 8 : 8);
+      p.K = kk;
+      p.KG = kk / 8;
+      p.slab_doubles = (size_t)p.K << N;
+      p.slots = (size_t)(((uint64_t)p.K * 2 * (1ull << (p.L - p.CB)) + p.unitsB - 1) / p.unitsB);
       p.staged = true;
-      p.KG = 1;
       p.amin = 1ull << p.L;
       if (p.slots < 4 * 160) p.slots = 4 * 160;
+      const char* la = getenv("SRE_LEGACY_A");
+      p.legacyA = la && la[0] == '1';
+      const char* lb = getenv("SRE_LEGACY_B");
+      p.legacyB = lb && lb[0] == '1';
     }
     if (p.L == 10) {  // staged pass A + persistent pass B (N = 15..20)
       p.staged = true;
@@ -178,26 +181,22 @@ int make_plan(int N, const Dev& d, Plan& p, uint64_t count = ~0ull) {
       if (p.slots < 4 * 160) p.slots = 4 * 160;  // persistent grids: <= 4 CTAs x SMs
       p.amin = 1024;
     }
-    if ((N == 19 || N == 20) && tmem_enabled()) {
-      p.tmem = true;
-      p.amin = N == 20 ? 2048 : 1024;
-    }
   }
   (void)d;
   return SRE_OK;
 }
 
 // Workspace layout (bytes, every region 256-B aligned for bulk copies):
-//   [partial slots][slab][norm scratch][FusedCtl][psi as complex64 (FP32 mode only)]
+//   [partial slots][slab][norm scratch][Ctl][psi as complex64 (FP32 mode only)]
 constexpr size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 size_t off_slab(const Plan& p, int B) { return align256(p.slots * NACC * (p.kind == TWOPASS ? 1 : (size_t)B) * 8); }
 size_t off_norm(const Plan& p, int B) { return off_slab(p, B) + align256(p.slab_doubles * 8); }
 size_t off_ctl(const Plan& p, int B) { return off_norm(p, B) + align256((4096 * (size_t)B + (size_t)B) * 8); }
-size_t off_psi32(const Plan& p, int B) { return off_ctl(p, B) + align256(sizeof(FusedCtl)); }
+size_t off_psi32(const Plan& p, int B) { return off_ctl(p, B) + align256(sizeof(Ctl)); }
 size_t ws_bytes_for(const Plan& p, int B, int prec = 0) {
   return off_psi32(p, B) + (prec ? align256(((size_t)B << p.N) * sizeof(float2)) : 0);
 }
-FusedCtl* ctl_of(char* ws, const Plan& p, int B) { return reinterpret_cast<FusedCtl*>(ws + off_ctl(p, B)); }
+Ctl* ctl_of(char* ws, const Plan& p, int B) { return reinterpret_cast<Ctl*>(ws + off_ctl(p, B)); }
 float2* psi32_of(char* ws, const Plan& p, int B) { return reinterpret_cast<float2*>(ws + off_psi32(p, B)); }
 
 // ------------------------------------------------------------------------------------------
@@ -239,11 +238,6 @@ std::vector<Sweep> make_sweeps(const double* alpha, int n_alpha) {
   return sw;
 }
 
-bool fused_enabled() {  // opt-in (SRE_FUSED=1): measured slower than the two staged launches
-  const char* e = getenv("SRE_FUSED");
-  return e && e[0] == '1';
-}
-
 int occupancy_small(int T, const Dev& d) {
   (void)T;
   return 4 * d.sms;  // 256-thread CTAs, modest registers
@@ -257,11 +251,10 @@ template <class V>
 int run_range_t(const typename Cx<V>::T* psi, const Plan& p, const Dev& d, int N, int B, uint64_t a_begin,
                 uint64_t a_end, const double* alpha, int n_alpha, char* ws, double* sums_dev, cudaStream_t st,
                 unsigned long long* hist = nullptr) {
-  constexpr bool F64 = std::is_same<V, double>::value;
   double* partial = reinterpret_cast<double*>(ws);
   V* slab = reinterpret_cast<V*>(ws + off_slab(p, B));
-  FusedCtl* ctl = ctl_of(ws, p, B);
-  CK(cudaMemsetAsync(ctl, 0, sizeof(FusedCtl), st));
+  Ctl* ctl = ctl_of(ws, p, B);
+  CK(cudaMemsetAsync(ctl, 0, sizeof(Ctl), st));
   const uint64_t count = a_end - a_begin;
   CK(cudaMemsetAsync(sums_dev, 0, sizeof(double) * (size_t)B * (n_alpha + 2), st));
   if (count == 0) return SRE_OK;
@@ -324,22 +317,6 @@ int run_range_t(const typename Cx<V>::T* psi, const Plan& p, const Dev& d, int N
           int rc2 = generic(a_begin, s0);
           if (rc2) return rc2;
           const uint64_t per = (uint64_t)8 * p.KG;
-          if constexpr (F64) {   // FP64-only experimental paths
-            if (fused_enabled() && p.L == 10 && s0 < a_end) {   // one persistent launch for the aligned bulk
-              cudaError_t e = sw.a2 ? launch_fused<true>(p, d, ps, s0, a_end - s0, slab, ctl, al_h, partial, st)
-                                    : launch_fused<false>(p, d, ps, s0, a_end - s0, slab, ctl, al_h, partial, st);
-              if (e != cudaSuccess) return fail(SRE_ECUDA, "fused: %s", cudaGetErrorString(e));
-              s0 = a_end;
-            }
-            if (p.tmem) {
-              for (uint64_t a = s0; a < a_end; a += per) {
-                const int kc = (int)((a_end - a) < per ? (a_end - a) : per);
-                cudaError_t e = launch_tmem_pair(p, d, sw.a2, ps, a, kc, slab, al_h, partial, st);
-                if (e != cudaSuccess) return fail(SRE_ECUDA, "tmem pair: %s", cudaGetErrorString(e));
-              }
-              s0 = a_end;
-            }
-          }
           for (uint64_t a = s0; a < a_end; a += per) {
             const int kc = (int)((a_end - a) < per ? (a_end - a) : per);
             cudaError_t e = launch_passA10s<V>(p, d, ps, a, kc, slab, st);
@@ -753,7 +730,6 @@ int sre_pauli_spectrum(const void* psi, int N, uint64_t a_begin, uint64_t a_end,
   const uint64_t count = a_end - a_begin;
   if (count == 0) return SRE_OK;
   if (p.kind == TWOPASS) {   // pass-B epilogues bin the final values; sums go to a scratch tail
-    if (fused_enabled() || p.tmem) return fail(SRE_EINVAL, "spectrum needs the default kernels (unset SRE_FUSED/SRE_TMEM)");
     const size_t need = ws_bytes_for(p, 1) + 256;
     if (ws_bytes < need) return fail(SRE_EWORKSPACE, "workspace %zu < required %zu", ws_bytes, need);
     double* scratch = reinterpret_cast<double*>(reinterpret_cast<char*>(workspace) + ws_bytes_for(p, 1));

@@ -22,7 +22,6 @@
 #include <cuda_runtime.h>
 #include <type_traits>
 
-#include "tmem.cuh"
 
 namespace sre {
 
@@ -600,15 +599,6 @@ __global__ void __launch_bounds__(TP >= 14 ? 512 : 256, 1) k_passB(int N, int L,
 // the staged rows (q = row[y_l], r = partner_row[y_l ^ a_l]), transforms 10 bits with one
 // warp-local exchange, and writes its row of both planes.  Items = (group, row).
 // ------------------------------------------------------------------------------------------
-// Chunk-major workspace for the TMEM pass B (H = 8): within a plane, position group
-// g = pos >> 7 (128 positions), then chunk c = y_h & 7, then m = y_h >> 3, then pos & 127.
-// A pass-B chunk (rows {c + 8m}, one 128-position group) is one contiguous 32 KB block.
-__device__ __forceinline__ size_t cm_row_off(uint64_t yh) { return (size_t)(((yh & 7) << 5) | (yh >> 3)) << 7; }
-template <int J>   // offset of position lane + 32 J (+ 1024 h) minus the lane: compile time
-__device__ __forceinline__ constexpr size_t cm_pos_off(int h) {
-  return ((size_t)((J >> 2) + 8 * h) << 15) + 32 * (J & 3);
-}
-
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gsrc) : "memory");
@@ -646,11 +636,11 @@ constexpr int PA10_SMEM = PA10_NS * 2 * 1024 * 16 + 8 * padded(1024) * 8;  // 12
 // finish with a ring slot refills it with the item NS positions ahead.  Warp w generates
 // X-string 8g + w from the staged rows, transforms 10 bits (one warp-local exchange per
 // plane) and writes its row of both planes.
-template <int N, bool RM = false, class V = double>   // RM: chunk-major workspace for the TMEM pass B
+template <int N, class V = double>
 __global__ void __launch_bounds__(256, 1) k_passA10s(const typename Cx<V>::T* __restrict__ psi, uint64_t a_first,
                                                      int kcount, int groups, V* __restrict__ ws) {
   using C2 = typename Cx<V>::T;
-  constexpr int cb = RM ? 10 : 12 - (N - 11);                   // pass B tile = 2^12 values
+  constexpr int cb = 12 - (N - 11);                             // pass B tile = 2^12 values
   extern __shared__ __align__(128) double smem[];
   C2* ring = reinterpret_cast<C2*>(smem);                       // [NS][q row | r row][1024]
   V* exch = reinterpret_cast<V*>(smem + PA10_NS * 2 * 1024 * 2);   // [warp][padded 1024]
@@ -712,19 +702,7 @@ __global__ void __launch_bounds__(256, 1) k_passA10s(const typename Cx<V>::T* __
     }
     if (active) {
       Rounds<10, 0, 0, 2, BarWarp, true, V>::run(v, xw, lane, BarWarp{});
-      // slab-major workspace: (y_h, pos) -> ((pos >> cb) << (H + cb)) | (y_h << cb) | (pos & (C-1));
-      // RM (TMEM pass B, H = 8): chunk-major ((pos >> 7) << 15) + row_off(y_h) + (pos & 127)
-      if constexpr (RM) {
-        static_assert(H == 8, "chunk-major layout assumes H = 8");
-        V* w1 = ws + (size_t)k * 2 * plane + cm_row_off(yh) + lane;
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const size_t o = ((size_t)(j >> 2) << 15) + 32 * (j & 3);
-          __stcg(w1 + o, v[0][j]);
-          __stcg(w1 + plane + o, v[1][j]);
-        }
-        continue;
-      }
+      // slab-major workspace: (y_h, pos) -> ((pos >> cb) << (H + cb)) | (y_h << cb) | (pos & (C-1))
       V* w0 = ws + (size_t)k * 2 * plane + (yh << cb);
       constexpr uint32_t cm = (1u << cb) - 1u;
 #pragma unroll
@@ -920,478 +898,319 @@ __global__ void __launch_bounds__(256, 1) k_passAs(const typename Cx<V>::T* __re
 }
 
 // ------------------------------------------------------------------------------------------
-// k_fused: the whole two-pass sweep for N = 15..20 in ONE persistent launch (grid = #SMs,
-// cooperative so every CTA is resident).  Each CTA runs two roles concurrently:
-//   warps 0-3 ("A"): items (batch b, row y_h); a batch is 4 consecutive X-strings sharing a_h;
-//                    the two psi rows arrive by bulk copy in a ring shared by the 4 warps;
-//                    warp w generates X-string 4b + w and transforms the 10 low bits
-//                    (same arithmetic as k_passA10s), writing the slab-major workspace slot b%S.
-//   warps 4-7 ("B"): one 128-thread unit; tiles (batch b, plane, slab) of 2^12 doubles arrive by
-//                    bulk copy (same arithmetic as k_passBt) and go through the H row bits and
-//                    the epilogue.
-// Work comes from two global tickets (in order), and the only waits are on earlier work:
-//   A-item of batch b waits until every B-tile of batch b - S has been copied in (slot reuse);
-//   B-tile of batch b waits until every A-item of batch b has been written.
-// Waits spin on L2 counters with acquire loads and a 10 s watchdog that records an error.
+// Tensor memory (TMEM) as a per-thread register extension.  Thread lane of warp w owns TMEM
+// lane 32 (w % 4) + lane; a double occupies two consecutive 32-bit columns.  tcgen05.ld/st
+// run on the tensor-memory datapath, not on the L1TEX data pipe the transposes saturate.
 // ------------------------------------------------------------------------------------------
-struct FusedCtl {              // zeroed by the host before each launch
-  unsigned long long a_next, b_next;
-  unsigned long long a_done[4], b_done[4];
-  int error;
-};
-constexpr int FZ_S = 2;                      // workspace slots (batches in flight)
-constexpr int FZ_KB = 4;                     // X-strings per batch (= A warps)
-constexpr int FZ_NSA = 3;                    // A staging ring depth (32 KB each)
-constexpr int FZ_NSB = 2;                    // B tile ring depth (33 KB each)
-constexpr int FZ_SMEM = FZ_NSA * 2048 * 16 + FZ_KB * padded(1024) * 8 + FZ_NSB * padded(4096) * 8;
-
-__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
-  return v;
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {   // one full warp
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n"
+               ::"r"(smem_u32(dst_smem)), "r"(ncols) : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
 }
-__device__ __forceinline__ void red_release_add(unsigned long long* p, unsigned long long v) {
-  asm volatile("red.release.gpu.global.add.u64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {      // same warp
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(taddr), "r"(ncols) : "memory");
 }
-__device__ __forceinline__ uint64_t gtimer() {
-  uint64_t t;
-  asm volatile("mov.u64 %0, %globaltimer;\n" : "=l"(t));
-  return t;
+__device__ __forceinline__ void tmem_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+// 8 doubles -> columns [ta, ta + 16) of this thread's lane
+__device__ __forceinline__ void tmem_st8d(uint32_t ta, const double (&v)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%16], {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15};\n"
+               ::"r"(__double2loint(v[0])), "r"(__double2hiint(v[0])), "r"(__double2loint(v[1])), "r"(__double2hiint(v[1])),
+                 "r"(__double2loint(v[2])), "r"(__double2hiint(v[2])), "r"(__double2loint(v[3])), "r"(__double2hiint(v[3])),
+                 "r"(__double2loint(v[4])), "r"(__double2hiint(v[4])), "r"(__double2loint(v[5])), "r"(__double2hiint(v[5])),
+                 "r"(__double2loint(v[6])), "r"(__double2hiint(v[6])), "r"(__double2loint(v[7])), "r"(__double2hiint(v[7])),
+                 "r"(ta) : "memory");
 }
-// spin until *p >= target; false (and ctl->error set) on a 10 s timeout
-__device__ __forceinline__ bool wait_geq(const unsigned long long* p, unsigned long long target, FusedCtl* ctl) {
-  if (ld_acquire(p) >= target) return true;
-  const uint64_t t0 = gtimer();
-  while (ld_acquire(p) < target) {
-    __nanosleep(200);
-    if (gtimer() - t0 > 10000000000ull || *(volatile int*)&ctl->error) { atomicExch(&ctl->error, 1); return false; }
-  }
-  return true;
+// columns [ta, ta + 16) -> 8 doubles (no wait: the caller issues tmem_wait_ld before use)
+__device__ __forceinline__ void tmem_ld8d(uint32_t ta, uint32_t (&u)[16]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];\n"
+               : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7]),
+                 "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]), "=r"(u[14]), "=r"(u[15])
+               : "r"(ta) : "memory");
+}
+__device__ __forceinline__ void stg_v4(double* p, double a, double b, double c, double d) {   // one 32-B sector
+  asm volatile("st.global.cg.v4.f64 [%0], {%1, %2, %3, %4};\n" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
 }
 
-template <int N, bool A2>
-__global__ void __launch_bounds__(256, 1) k_fused(const double2* __restrict__ psi, uint64_t a_first, uint64_t count,
-                                                  double* __restrict__ ws, FusedCtl* ctl, Alphas al, double* partial) {
-  constexpr int H = N - 11, CB = 12 - H, TP = 12, TILE = 1 << TP;
-  constexpr uint64_t ROWS = 1ull << H;
-  constexpr uint64_t SLABS = 1ull << (10 - CB);
-  constexpr uint64_t TPB = (uint64_t)FZ_KB * 2 * SLABS;   // B tiles per full batch
-  constexpr size_t PLANE = (size_t)1 << (N - 1);
-  constexpr size_t SLOT = (size_t)FZ_KB * 2 * PLANE;     // doubles per workspace slot
-  constexpr uint64_t END = ~0ull;
-  extern __shared__ __align__(128) double smem[];
-  double2* ringA = reinterpret_cast<double2*>(smem);                          // [NSA][2048]
-  double* exA = smem + FZ_NSA * 2048 * 2;                                     // [4][padded 1024]
-  double* ringB = exA + FZ_KB * padded(1024);                                 // [NSB][padded 4096]
-  __shared__ __align__(8) uint64_t fullA[FZ_NSA], fullB[FZ_NSB];
-  __shared__ uint64_t itemA[FZ_NSA], itemB[FZ_NSB];
-  __shared__ int usedA[FZ_NSA];
-  __shared__ double redB[4][NACC];
-  const uint64_t nbatch = (count + FZ_KB - 1) / FZ_KB;
-  const uint64_t totA = nbatch * ROWS;
-  const uint64_t totB = (count / FZ_KB) * TPB + (count % FZ_KB) * 2 * SLABS;
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < FZ_NSA; ++i) { mbar_init(&fullA[i], 1); usedA[i] = 0; }
-    for (int i = 0; i < FZ_NSB; ++i) mbar_init(&fullB[i], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  __syncthreads();
-
-  // A producer (one thread, never waits): next A ticket into ring slot s, stage its psi rows
-  auto produceA = [&](int s) {
-    const uint64_t t = atomicAdd(&ctl->a_next, 1ull);
-    if (t >= totA) {
-      itemA[s] = END;
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&fullA[s])) : "memory");
-      return;
+// 64-point radix-2 butterflies over the register index (6 stages, pure DADD)
+__device__ __forceinline__ void bfly64(double (&v)[64]) {
+#pragma unroll
+  for (int h = 1; h < 64; h <<= 1)
+#pragma unroll
+    for (int i = 0; i < 64; ++i) {
+      if (i & h) continue;
+      const double a = v[i], b = v[i + h];
+      v[i] = a + b;
+      v[i + h] = a - b;
     }
-    const uint64_t b = t >> H, yh = t & (ROWS - 1);
-    const uint64_t ag = a_first + FZ_KB * b;
-    const int p = 63 - __clzll((long long)ag);
-    const uint64_t xh = ins0(yh, p - 10);
-    itemA[s] = t;
-    double2* dst = ringA + (size_t)s * 2048;
-    mbar_expect_tx(&fullA[s], 2 * 1024 * 16);
-    bulk_g2s(dst, psi + (xh << 10), 1024 * 16, &fullA[s]);
-    bulk_g2s(dst + 1024, psi + ((xh ^ (ag >> 10)) << 10), 1024 * 16, &fullA[s]);
-  };
-
-  if (w < 4) {
-    // ======================= A role =======================
-    if (threadIdx.x == 0)
-      for (int s = 0; s < FZ_NSA; ++s) produceA(s);
-    double* xw = exA + (size_t)w * padded(1024);
-    for (uint32_t n = 0;; ++n) {
-      const int s = (int)(n % FZ_NSA);
-      mbar_wait(&fullA[s], (n / FZ_NSA) & 1u);
-      const uint64_t t = itemA[s];
-      if (t == END) break;
-      const uint64_t b = t >> H, yh = t & (ROWS - 1);
-      const uint64_t kglob = FZ_KB * b + w;
-      const bool active = kglob < count;
-      double v[2][32];
-      if (active) {
-        const uint32_t alow = (uint32_t)((a_first + kglob) & 1023u);
-        const double2* sq = ringA + (size_t)s * 2048;
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const uint32_t yl = lane + 32 * j;
-          const double2 q = sq[yl];
-          const double2 r = sq[1024 + (yl ^ alow)];
-          v[0][j] = fma(r.x, q.x, r.y * q.y);
-          v[1][j] = fma(r.x, q.y, -(r.y * q.x));
-        }
-        Rounds<10, 0, 0, 2, BarWarp, true>::run(v, xw, lane, BarWarp{});
-        // workspace slot b%S is free once every B tile of batch b - S has been copied out
-        if (b >= FZ_S && lane == 0) wait_geq(&ctl->b_done[b % FZ_S], (b / FZ_S) * TPB, ctl);
-        __syncwarp();
-        double* w0 = ws + (b % FZ_S) * SLOT + (size_t)w * 2 * PLANE + (yh << CB);
-        constexpr uint32_t cm = (1u << CB) - 1u;
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const uint32_t pos = lane + 32 * j;
-          const size_t off = ((size_t)(pos >> CB) << (H + CB)) + (pos & cm);
-          __stcg(w0 + off, v[0][j]);
-          __stcg(w0 + PLANE + off, v[1][j]);
-        }
-        __threadfence();
-      }
-      __syncwarp();
-      if (lane == 0) {
-        // the last of the 4 warps to finish this item publishes it and refills the ring slot
-        if (atomicAdd(&usedA[s], 1) == FZ_KB - 1) {
-          atomicExch(&usedA[s], 0);
-          __threadfence();
-          red_release_add(&ctl->a_done[b % FZ_S], 1ull);
-          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-          produceA(s);
-        }
-      }
-    }
-  } else {
-    // ======================= B role =======================
-    const uint32_t tb = threadIdx.x - 128;
-    const BarNamed bar{1, 128};
-    double acc[NACC];
-#pragma unroll
-    for (int i = 0; i < NACC; ++i) acc[i] = 0.0;
-    // Leader-only producer state.  positions [0, issued) are staged; [0, credited) have been
-    // credited to b_done (their copy has landed, so the workspace slot no longer needs them).
-    // A claimed tile may have to wait for its batch; before the leader waits it credits every
-    // staged position, so nothing another warp waits on is ever held back by that wait.
-    uint32_t issued = 0, credited = 0;
-    bool ended = false;
-    auto credit_upto = [&](uint32_t upto) {
-      for (; credited < upto; ++credited) {
-        const int cs = (int)(credited % FZ_NSB);
-        mbar_wait(&fullB[cs], (credited / FZ_NSB) & 1u);
-        const uint64_t ct = itemB[cs];
-        if (ct != END) red_release_add(&ctl->b_done[(ct / TPB) % FZ_S], 1ull);
-      }
-    };
-    auto produce_upto = [&](uint32_t upto) {     // fill positions [issued, upto)
-      while (issued < upto && !ended) {
-        const int ps = (int)(issued % FZ_NSB);
-        const uint64_t t = atomicAdd(&ctl->b_next, 1ull);
-        if (t >= totB) {
-          itemB[ps] = END;
-          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&fullB[ps])) : "memory");
-          ++issued;
-          ended = true;
-          return;
-        }
-        const uint64_t b = t / TPB;
-        const unsigned long long need = (b / FZ_S + 1) * ROWS;
-        if (ld_acquire(&ctl->a_done[b % FZ_S]) < need) {
-          credit_upto(issued);
-          if (!wait_geq(&ctl->a_done[b % FZ_S], need, ctl)) {
-            itemB[ps] = END;
-            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&fullB[ps])) : "memory");
-            ++issued;
-            ended = true;
-            return;
-          }
-        }
-        asm volatile("fence.proxy.async.global;\n" ::: "memory");
-        itemB[ps] = t;
-        mbar_expect_tx(&fullB[ps], TILE * 8);
-        bulk_g2s(ringB + (size_t)ps * padded(TILE), ws + (b % FZ_S) * SLOT + (t % TPB) * TILE, TILE * 8, &fullB[ps]);
-        ++issued;
-      }
-    };
-    for (uint32_t n = 0;; ++n) {
-      const int s = (int)(n % FZ_NSB);
-      if (tb == 0) {
-        produce_upto(n + FZ_NSB);
-        credit_upto(n + 1);                      // this position's copy has landed
-      }
-      mbar_wait(&fullB[s], (n / FZ_NSB) & 1u);
-      const uint64_t t = itemB[s];
-      if (t == END) break;
-      double* buf = ringB + (size_t)s * padded(TILE);
-      double v[1][32];
-#pragma unroll
-      for (int j = 0; j < 32; ++j) v[0][j] = buf[tb + 128 * j];
-      Rounds<TP, CB, 0, 1, BarNamed>::run(v, buf, tb, bar);
-      bar.sync();                                // the slot's smem is free for the next copy
-      if (tb == 0) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      tile_accumulate<A2>(acc, v[0], al);
-    }
-    // B-role accumulators -> partial[blockIdx.x]
-#pragma unroll
-    for (int i = 0; i < NACC; ++i) {
-      double x = acc[i];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-      if (lane == 0) redB[w - 4][i] = x;
-    }
-    bar.sync();
-    if (tb < NACC) {
-      double sacc = 0.0;
-      for (int k = 0; k < 4; ++k) sacc += redB[k][tb];
-      partial[(size_t)blockIdx.x * NACC + tb] += sacc;
-    }
-  }
 }
 
-// ==========================================================================================
-// TMEM path for N = 19, 20 (T = N-1 = L + 8).  Pass B gives every thread one workspace column of
-// 2^8 rows held in tensor memory, so the 8 row bits are transformed inside the thread with no
-// shared-memory exchange; pass A (L = 11 at N = 20) parks one plane in TMEM so a warp can own
-// 64 values per plane per lane (6 in-thread bits).  L1TEX data-pipe traffic per output value:
-// 16 B generation + 16 B exchange + 8 B store (A) + 8 B load (B) = 48 B.
-// Workspace: row-major planes [k][plane][y_h][pos], 2^L positions per row; pos low 5 bits are
-// y_l bits 5..9 (the lane index of pass A's final layout), so both passes access it coalesced.
-// ==========================================================================================
-// 32x32 transpose of one value per (lane, j) through a warp-private padded buffer:
-// element e = lane + 32 j is read back as e = j + 32 lane (conflict-free both ways)
-__device__ __forceinline__ void warp_transpose32(double (&v)[32], double* xw, int lane) {
-  __syncwarp();
-#pragma unroll
-  for (int j = 0; j < 32; ++j) xw[swz(lane + 32 * j)] = v[j];
-  __syncwarp();
-#pragma unroll
-  for (int j = 0; j < 32; ++j) v[j] = xw[swz(j + 32 * lane)];
+// ------------------------------------------------------------------------------------------
+// Radix-64 streamed pass A for L = 12 (N = 21..24), FP64: k_passAq.
+// A 4096-point plane row is held by a unit of 64 threads x 64 values, so the 12 low bits take two
+// register rounds and ONE shared-memory transpose (k_passAs: 32 values per thread, three rounds).
+//   CTA = 4 units (256 threads); an item is (block of 4 consecutive rows 4m..4m+3, X-string k);
+//   unit u transforms row 4m + u.  Each unit streams its two psi rows (x_h = ins0(y_h, p - 12) and
+//   x_h ^ a_h) in 16 chunks of 256 complex (q chunk c, r chunk c ^ (a_l >> 8): 8 KB per stage) through
+//   its own 3-deep bulk-copy ring.  Generation computes both planes; plane A stays in registers,
+//   plane B is parked in TMEM (128 columns per thread) until plane A is stored.
+//   Round 0: register index j = pos bits 6..11 (pos = t + 64 j).  Transpose through the unit's
+//   32 KB XOR-swizzled buffer (physical = e ^ ((e >> 6) & 15): conflict-free both ways, no pad).
+//   Round 1: j = pos bits 0..5 (pos = 64 t + j).
+//   Store: the 4 rows are staged in the CTA's 128 KB (the four transpose buffers) in workspace
+//   order -- per slab of 2^CB columns, rows 4m..4m+3 are contiguous in the slab-major workspace of
+//   k_passBt<13, CB = 13 - H>, i.e. 4 x 2^CB x 8 B (>= one 128-B line) per slab -- and written
+//   back with coalesced 16-B stores, every warp instruction covering whole lines.  Measured on B200
+//   (tools/microbench_wr.cu, N = 24): 32-B runs written one row at a time reach 1.9-2.2 TB/s of
+//   HBM, whole 4-row lines 4.5 TB/s.
+// Items run X-string-fastest, so the K X-strings of a launch read each psi row pair from L2 after
+// its first HBM fetch.
+// ------------------------------------------------------------------------------------------
+constexpr int PAQ_NS = 3;                                             // ring stages per unit
+constexpr int PAQ_CH = 256;                                           // complex per chunk
+constexpr int PAQ_SMEM = 4 * PAQ_NS * 2 * PAQ_CH * 16 + 4 * 4096 * 8;  // 96 KB rings + 128 KB transposes
+__device__ __forceinline__ uint32_t xsw12(uint32_t e) { return e ^ ((e >> 6) & 15u); }
+__device__ __forceinline__ uint32_t xsw16(uint32_t c) { return c ^ ((c >> 7) & 7u); }   // 16-B chunks of the staging
+__device__ __forceinline__ void tmem_st4d(uint32_t ta, const double (&v)[4]) {         // 4 doubles -> 8 columns
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%8], {%0, %1, %2, %3, %4, %5, %6, %7};\n"
+               ::"r"(__double2loint(v[0])), "r"(__double2hiint(v[0])), "r"(__double2loint(v[1])), "r"(__double2hiint(v[1])),
+                 "r"(__double2loint(v[2])), "r"(__double2hiint(v[2])), "r"(__double2loint(v[3])), "r"(__double2hiint(v[3])),
+                 "r"(ta) : "memory");
 }
-
-constexpr int PA11_NS = 2;                                                   // staging ring depth
-constexpr int PA11_SMEM = PA11_NS * 2 * 2048 * 16 + 8 * padded(1024) * 8;   // 128 KB ring + 66 KB exchange
 
 template <int N>
-__global__ void __launch_bounds__(256, 1) k_passA11t(const double2* __restrict__ psi, uint64_t a_first, int kcount,
-                                                     int groups, double* __restrict__ ws) {
-  constexpr int L = 11, H = N - 1 - L;
-  constexpr uint64_t ROWS = 1ull << H;
+__global__ void __launch_bounds__(256, 1) k_passAq(const double2* __restrict__ psi, uint64_t a_first, int kcount,
+                                                   double* __restrict__ ws) {
+  constexpr int L = 12, H = N - 1 - L, CB = 13 - H;
+  static_assert(H >= 8 && H <= 11, "k_passAq covers N = 21..24");
+  constexpr uint64_t RBLK = 1ull << (H - 2);                          // 4-row blocks per plane
   constexpr size_t PLANE = (size_t)1 << (N - 1);
+  constexpr int QB = CB - 2;                                          // 32-B pieces per slab row = 2^QB
   extern __shared__ __align__(128) double smem[];
-  double2* ring = reinterpret_cast<double2*>(smem);             // [NS][q row | r row][2048]
-  double* exch = smem + PA11_NS * 2 * 2048 * 2;                 // [warp][padded 1024]
-  __shared__ __align__(8) uint64_t full[PA11_NS];
-  __shared__ int used[PA11_NS];
-  __shared__ uint32_t tbase;
+  double2* rings = reinterpret_cast<double2*>(smem);                 // [unit][NS][q 256 | r 256]
+  double* exch = smem + 4 * PAQ_NS * 2 * PAQ_CH * 2;                  // [unit][4096]; all four = staging
+  __shared__ __align__(8) uint64_t full[4][PAQ_NS];
+  __shared__ int used[4][PAQ_NS];
+  __shared__ uint32_t tmem_s;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint64_t items = ROWS * (uint64_t)groups;
-  if (w == 0) tmem_alloc_warp(&tbase, 512);
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < PA11_NS; ++i) { mbar_init(&full[i], 1); used[i] = 0; }
+  const int u = w >> 1;
+  const uint32_t t = threadIdx.x & 63;
+  const uint64_t items = RBLK * (uint64_t)kcount;
+  const uint64_t my_items = items > blockIdx.x ? (items - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const uint64_t stages = my_items * 16;
+  if (w == 0) tmem_alloc(&tmem_s, 256);
+  if (threadIdx.x == 32) {
+    for (int x = 0; x < 4; ++x)
+      for (int i = 0; i < PAQ_NS; ++i) { mbar_init(&full[x][i], 1); used[x][i] = 0; }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
-  // this warp's TMEM: lanes 32*(w%4).., columns (w/4)*256 ..; chunks A0 @0, B0 @64, B1 @128
-  const uint32_t tw = tbase + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)(w >> 2) * 256;
-  auto issue = [&](uint64_t item, int slot) {
-    const uint64_t g = item >> H, yh = item & (ROWS - 1);
-    const uint64_t ag = a_first + 8 * g;
-    const int p = 63 - __clzll((long long)ag);                  // >= 11 (a >= 2048)
-    const uint64_t xh = ins0(yh, p - L);
-    double2* dst = ring + (size_t)slot * 4096;
-    mbar_expect_tx(&full[slot], 2 * 2048 * 16);
-    bulk_g2s(dst, psi + (xh << L), 2048 * 16, &full[slot]);
-    bulk_g2s(dst + 2048, psi + ((xh ^ (ag >> L)) << L), 2048 * 16, &full[slot]);
+  const uint32_t tm = tmem_s + ((uint32_t)(32 * (w & 3)) << 16) + 128u * (uint32_t)(w >> 2);
+  double2* ring = rings + (size_t)u * PAQ_NS * 2 * PAQ_CH;
+  auto produce = [&](uint64_t s, int slot) {                        // one thread of unit u
+    const uint64_t item = blockIdx.x + (s >> 4) * gridDim.x;
+    const uint32_t c = (uint32_t)(s & 15);
+    const uint64_t m = item / (uint64_t)kcount;
+    const uint64_t a = a_first + item % (uint64_t)kcount;
+    const int p = 63 - __clzll((long long)a);                        // >= 12
+    const uint64_t xh = ins0(4 * m + u, p - L);
+    const uint32_t ahi = (uint32_t)((a >> 8) & 15u);
+    double2* dst = ring + (size_t)slot * 2 * PAQ_CH;
+    mbar_expect_tx(&full[u][slot], 2 * PAQ_CH * sizeof(double2));
+    bulk_g2s(dst, psi + (xh << L) + PAQ_CH * c, PAQ_CH * sizeof(double2), &full[u][slot]);
+    bulk_g2s(dst + PAQ_CH, psi + ((xh ^ (a >> L)) << L) + PAQ_CH * (c ^ ahi), PAQ_CH * sizeof(double2), &full[u][slot]);
   };
-  if (threadIdx.x == 0)
-    for (int i = 0; i < PA11_NS; ++i)
-      if (blockIdx.x + (uint64_t)i * gridDim.x < items) issue(blockIdx.x + (uint64_t)i * gridDim.x, i);
-  double* xw = exch + (size_t)w * padded(1024);
-  uint32_t n = 0;
-  for (uint64_t item = blockIdx.x; item < items; item += gridDim.x, ++n) {
-    const int slot = (int)(n % PA11_NS);
-    mbar_wait(&full[slot], (n / PA11_NS) & 1u);
-    const uint64_t g = item >> H, yh = item & (ROWS - 1);
-    const int k = 8 * (int)g + w;
-    const bool active = k < kcount;
-    double lo[32], hi[32];
-    if (active) {
-      const uint32_t al = (uint32_t)((a_first + (uint64_t)k) & 2047u);
-      const double2* sq = ring + (size_t)slot * 4096;
-      // chunk c: y_l = lane + 32 j + 1024 c; registers j <-> y bits 5..9
+  if (t == 0)
+    for (int i = 0; i < PAQ_NS; ++i)
+      if ((uint64_t)i < stages) produce(i, i);
+  double* xb = exch + (size_t)u * 4096;
+  const BarNamed bar{1 + u, 64};
+  uint64_t s = 0;
+  for (uint64_t li = 0; li < my_items; ++li) {
+    const uint64_t item = blockIdx.x + li * gridDim.x;
+    const uint64_t m = item / (uint64_t)kcount;
+    const uint64_t k = item % (uint64_t)kcount;
+    const uint32_t al = (uint32_t)((a_first + k) & 4095u);
+    const uint32_t alo = al & 63u, ajq = (al >> 6) & 3u;
+    double v[64];
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        double A[32], B[32];
+    for (int c = 0; c < 16; ++c, ++s) {
+      const int slot = (int)(s % PAQ_NS);
+      mbar_wait(&full[u][slot], (uint32_t)(s / PAQ_NS) & 1u);
+      const double2* cq = ring + (size_t)slot * 2 * PAQ_CH;
+      double b4[4];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const uint32_t yl = lane + 32 * j + 1024 * c;
-          const double2 q = sq[yl];
-          const double2 r = sq[2048 + (yl ^ al)];
-          A[j] = fma(r.x, q.x, r.y * q.y);
-          B[j] = fma(r.x, q.y, -(r.y * q.x));
-        }
-        bfly32<0, 5>(A);
-        bfly32<0, 5>(B);
-        if (c == 0) {
-          tmem_st32(tw + 0, A);
-          tmem_st32(tw + 64, B);
-        } else {
-          tmem_st32(tw + 128, B);
-#pragma unroll
-          for (int j = 0; j < 32; ++j) hi[j] = A[j];
+      for (int i = 0; i < 4; ++i) {
+        const double2 q = cq[t + 64 * i];
+        const double2 r = cq[PAQ_CH + (t ^ alo) + 64 * (i ^ ajq)];
+        v[4 * c + i] = fma(r.x, q.x, r.y * q.y);        // Re conj(psi_{x^a}) psi_x
+        b4[i] = fma(r.x, q.y, -(r.y * q.x));            // Im
+      }
+      tmem_st4d(tm + 8u * c, b4);
+      __syncwarp();
+      if (lane == 0) {                                   // release the stage; the unit's 2nd warp refills it
+        if (atomicAdd(&used[u][slot], 1) == 1) {
+          atomicExch(&used[u][slot], 0);
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          if (s + PAQ_NS < stages) produce(s + PAQ_NS, slot);
         }
       }
     }
-    __syncwarp();
-    if (lane == 0 && atomicAdd(&used[slot], 1) == 7) {          // ring slot read out by all 8 warps
-      atomicExch(&used[slot], 0);
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      const uint64_t nx = item + (uint64_t)PA11_NS * gridDim.x;
-      if (nx < items) issue(nx, slot);
-    }
-    if (active) {
-      tmem_wait_st();
+    tmem_wait_st();
+    double* wk = ws + (size_t)k * 2 * PLANE + (m << (CB + 2));         // rows 4m.. of slab 0
+    auto transform_store = [&](double* wp) {
+      bfly64(v);                                         // round 0: pos bits 6..11
+      bar.sync();                                        // previous readers of xb are done
 #pragma unroll
-      for (int pl = 0; pl < 2; ++pl) {
-        if (pl == 0) tmem_ld32(tw + 0, lo);                     // A0; A1 is already in hi
-        else { tmem_ld32(tw + 64, lo); tmem_ld32(tw + 128, hi); }
+      for (int j = 0; j < 64; ++j) xb[xsw12(t + 64u * j)] = v[j];
+      bar.sync();
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {                          // y bit 10
-          const double u = lo[j], v2 = hi[j];
-          lo[j] = u + v2;
-          hi[j] = u - v2;
-        }
-        // exchange each half: (lane <-> y bits 0-4, j <-> 5-9) -> (lane <-> 5-9, j <-> 0-4)
-        warp_transpose32(lo, xw, lane);
-        warp_transpose32(hi, xw, lane);
-        bfly32<0, 5>(lo);
-        bfly32<0, 5>(hi);
-        // position pos = lane + 32 j + 1024 h  (pos bits 0-4 = b_l bits 5-9, contiguous over lanes),
-        // stored chunk-major: ((pos >> 7) << 15) + row_off(y_h) + (pos & 127)
-        double* dst = ws + (size_t)k * 2 * PLANE + (size_t)pl * PLANE + cm_row_off(yh) + lane;
+      for (int j = 0; j < 64; ++j) v[j] = xb[xsw12(64u * t + j)];
+      bfly64(v);                                         // round 1: pos bits 0..5
+      // staging (16-B chunks, workspace order): piece g = (slab, row u, sub-piece q) of 4 doubles
+      __syncthreads();                                   // every unit is done with its transpose buffer
+      double2* st2 = reinterpret_cast<double2*>(exch);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const size_t o = ((size_t)(j >> 2) << 15) + 32 * (j & 3);
-          __stcg(dst + o, lo[j]);
-          __stcg(dst + (8ull << 15) + o, hi[j]);
-        }
+      for (int r = 0; r < 16; ++r) {
+        const uint32_t pc = 16u * t + r;                 // piece of this row: pos = 4 pc .. 4 pc + 3
+        const uint32_t g = (((pc >> QB) * 4u + (uint32_t)u) << QB) + (pc & ((1u << QB) - 1u));
+        st2[xsw16(2 * g)] = make_double2(v[4 * r], v[4 * r + 1]);
+        st2[xsw16(2 * g + 1)] = make_double2(v[4 * r + 2], v[4 * r + 3]);
       }
+      __syncthreads();
+      // chunk C -> piece g = C >> 1 -> (slab g >> (QB + 2), rows 4m.., offset within the slab's 4-row run)
+#pragma unroll 8
+      for (int i = 0; i < 32; ++i) {
+        const uint32_t C = threadIdx.x + 256u * i;
+        const uint32_t g = C >> 1;
+        const size_t off = ((size_t)(g >> (QB + 2)) << (H + CB)) + 4u * (g & ((4u << QB) - 1u)) + 2u * (C & 1u);
+        const double2 x = st2[xsw16(C)];
+        __stcg(reinterpret_cast<double2*>(wp + off), x);
+      }
+      __syncthreads();                                   // staging read by every unit before the next transpose
+    };
+    transform_store(wk);                                 // plane A
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {                        // plane B back from TMEM
+      uint32_t r32[16];
+      tmem_ld8d(tm + 16u * c, r32);
+      tmem_wait_ld();
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[8 * c + i] = __hiloint2double(r32[2 * i + 1], r32[2 * i]);
     }
+    transform_store(wk + PLANE);                         // plane B
   }
   tmem_fence_before();
   __syncthreads();
-  if (w == 0) tmem_dealloc_warp(tbase, 512);
+  if (w == 0) tmem_dealloc(tmem_s, 256);
 }
 
-// Pass B with the 8 row bits in TMEM: a CTA of 4 warps walks tiles (k, plane, 128-position
-// group); thread = one position (column), its 256 rows live in its TMEM lane (512 columns).
-// The tile streams in as 8 chunks (chunk c = rows {c + 8m}, m = 0..31) through a 4-deep ring of
-// 32 KB shared-memory buffers filled by bulk copies (one 1 KB row segment per lane), so global
-// latency is off the critical path.  Round 1: chunk c (row bits 3-7 in registers) is read from
-// shared memory, transformed and parked at TMEM columns 64c.  Round 2: groups of 4 m's across
-// the 8 chunks (row bits 0-2) come back from TMEM and feed the epilogue directly.
-constexpr int PB8_NS = 4;
-constexpr int PB8_SMEM = PB8_NS * 32 * 128 * 8;   // 4 x 32 KB
+// ------------------------------------------------------------------------------------------
+// Radix-64 pass B over 2^13-double tiles (N = 21..24, FP64): k_passBr<CB>.  A tile is the
+// contiguous slab of 2^H rows x 2^CB columns (H + CB = 13, element e = row * 2^CB + col) that
+// k_passAq wrote; a unit of 128 threads holds it as 64 values per thread, so the H row bits take
+// two register rounds and ONE transpose (k_passBt<13, CB>: 32 values, three rounds).
+//   Round 0: registers = e bits 7..12 (the 6 high row bits), thread = e bits 0..6 (pos = t + 128 j).
+//   Round 1: registers = e bits 1..6 (the remaining H - 6 row bits and CB - 1 column bits),
+//            thread = e bit 0 and e bits 7..12; the power sums accumulate from here.
+//   The transpose runs in place in the tile's ring slot with physical index
+//   e ^ (((e >> 7) & 7) << 1): both layouts are conflict-free (half-warps hit 16 distinct banks).
+// A CTA runs two units over three 64 KB slots: CTA tile n sits in slot n % 3 and belongs to unit
+// n % 2; a unit hands its slot back (refill with tile n + 3) right after its round-1 loads.
+// ------------------------------------------------------------------------------------------
+constexpr int PBR_SMEM = 3 * 8192 * 8;
+__device__ __forceinline__ uint32_t xsw13(uint32_t e) { return e ^ (((e >> 7) & 7u) << 1); }
 
-template <int N, bool A2>
-__global__ void __launch_bounds__(128, 1) k_passBt8(int kcount, const double* __restrict__ ws, Alphas al,
-                                                    double* partial) {
-  constexpr int H = 8, L = N - 1 - H;
-  constexpr size_t PLANE = (size_t)1 << (N - 1);
-  constexpr uint64_t GROUPS = 1ull << (L - 7);                  // 128-position groups per plane
-  extern __shared__ __align__(128) double smem[];               // [NS][32 rows][128 positions]
-  __shared__ __align__(8) uint64_t full[PB8_NS];
-  __shared__ int used[PB8_NS];
-  __shared__ uint32_t tbase;
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (w == 0) tmem_alloc_warp(&tbase, 512);
+template <int CB, bool A2>
+__global__ void __launch_bounds__(256, 1) k_passBr(int kcount, const double* __restrict__ ws, Alphas al,
+                                                   double* partial) {
+  constexpr int H = 13 - CB, L = 12;
+  static_assert(H >= 8 && H <= 11, "k_passBr covers N = 21..24");
+  extern __shared__ __align__(128) double smem[];
+  __shared__ __align__(8) uint64_t full[3];
+  __shared__ volatile unsigned long long issued[3];
+  __shared__ unsigned long long shist[SPEC_BINS];
+  const int u = threadIdx.x >> 7;
+  const uint32_t t = threadIdx.x & 127;
+  const uint64_t slabs = 1ull << (L - CB);
+  const uint64_t tiles = (uint64_t)kcount * 2 * slabs;
+  const uint64_t my_tiles = tiles > blockIdx.x ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const BarNamed bar{1 + u, 128};
   if (threadIdx.x == 0) {
-    for (int i = 0; i < PB8_NS; ++i) { mbar_init(&full[i], 1); used[i] = 0; }
+    for (int i = 0; i < 3; ++i) { mbar_init(&full[i], 1); issued[i] = ~0ull; }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  tmem_fence_before();
+  if (al.hist)
+    for (int i = threadIdx.x; i < SPEC_BINS; i += blockDim.x) shist[i] = 0ull;
   __syncthreads();
-  tmem_fence_after();
-  const uint32_t tw = tbase + ((uint32_t)(32 * w) << 16);
-  const uint64_t tiles = (uint64_t)kcount * 2 * GROUPS;
-  const uint64_t my_tiles = tiles > blockIdx.x ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const uint64_t nchunks = my_tiles * 8;                        // chunk n: tile blockIdx + (n/8) grid, c = n%8
-  // a chunk (rows {c + 8m} of one 128-position group) is one contiguous 32 KB block (chunk-major)
-  auto issue = [&](uint64_t nch, int slot) {
-    if (lane != 0) return;
-    const uint64_t tile = blockIdx.x + (nch >> 3) * gridDim.x;
-    const int c = (int)(nch & 7);
-    const uint64_t kp = tile / GROUPS, grp = tile % GROUPS;
-    mbar_expect_tx(&full[slot], 32 * 128 * 8);
-    bulk_g2s(smem + (size_t)slot * 4096, ws + kp * PLANE + (grp << 15) + ((size_t)c << 12), 32 * 128 * 8, &full[slot]);
+  // issued[slot] = the CTA tile whose copy targets the slot.  A unit may only wait on a slot's
+  // mbarrier once its own tile has been issued there: tile n - 3 (the previous occupant) belongs to
+  // the other unit, so without this check a fast unit could test the parity of a phase two
+  // completions ahead, read early, and have a second copy land in the same slot.
+  auto issue = [&](uint64_t n) {                                   // one thread
+    const int slot = (int)(n % 3);
+    issued[slot] = n;
+    mbar_expect_tx(&full[slot], 8192 * sizeof(double));
+    bulk_g2s(smem + (size_t)slot * 8192, ws + (blockIdx.x + n * gridDim.x) * 8192, 8192 * sizeof(double), &full[slot]);
   };
-  if (w == 0)
-    for (int i = 0; i < PB8_NS; ++i)
-      if ((uint64_t)i < nchunks) issue(i, i);
+  if (threadIdx.x == 0)
+    for (uint64_t n = 0; n < 3 && n < my_tiles; ++n) issue(n);
   double acc[NACC];
 #pragma unroll
   for (int i = 0; i < NACC; ++i) acc[i] = 0.0;
-  uint64_t n = 0;
-  for (uint64_t t = 0; t < my_tiles; ++t) {
-#pragma unroll 1
-    for (int c = 0; c < 8; ++c, ++n) {
-      const int slot = (int)(n % PB8_NS);
-      mbar_wait(&full[slot], (uint32_t)(n / PB8_NS) & 1u);
-      double v[32];
-      const double* buf = smem + (size_t)slot * 4096 + 32 * w + lane;
+  for (uint64_t n = (uint64_t)u; n < my_tiles; n += 2) {
+    const int slot = (int)(n % 3);
+    double* buf = smem + (size_t)slot * 8192;
+    while (issued[slot] != n) __nanosleep(32);
+    mbar_wait(&full[slot], (uint32_t)(n / 3) & 1u);
+    double v[64];
 #pragma unroll
-      for (int m = 0; m < 32; ++m) v[m] = buf[128 * m];
-      __syncwarp();
-      int last = 0;
-      if (lane == 0) last = atomicAdd(&used[slot], 1) == 3;     // last of the 4 warps to read it
-      if (__shfl_sync(0xffffffffu, last, 0)) {
-        if (lane == 0) atomicExch(&used[slot], 0);
-        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        if (n + PB8_NS < nchunks) issue(n + PB8_NS, slot);
-      }
-      bfly32<0, 5>(v);
-      tmem_st32(tw + 64 * c, v);
+    for (int j = 0; j < 64; ++j) v[j] = buf[t + 128u * j];      // round-0 layout, natural order
+    bfly64(v);                                                   // 6 high row bits
+    bar.sync();                                                  // every thread has read the tile
+#pragma unroll
+    for (int j = 0; j < 64; ++j) buf[xsw13(t + 128u * j)] = v[j];
+    bar.sync();
+    const uint32_t tb = (t & 1u) | ((t >> 1) << 7);
+#pragma unroll
+    for (int j = 0; j < 64; ++j) v[j] = buf[xsw13(tb | ((uint32_t)j << 1))];
+    bar.sync();                                                  // slot free
+    if (t == 0) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      if (n + 3 < my_tiles) issue(n + 3);
     }
-    tmem_wait_st();
-    double loc[NACC];
+    // round 1: register bits 0..5 = e bits 1..6; the low (H - 6) of them... all 6 are butterflied
+    // except the column bits (e bits < CB), which index independent columns
+    constexpr int CLO = CB - 1;                                  // column bits among register bits 0..5
 #pragma unroll
-    for (int i = 0; i < NACC; ++i) loc[i] = 0.0;
-#pragma unroll 1
-    for (int q = 0; q < 8; ++q) {
-      double u[32];                                             // u[4c + i] = row c + 8 (4q + i)
-      tmem_ld4x8(tw + 8 * q, u);
+    for (int h = 1 << CLO; h < 64; h <<= 1)
 #pragma unroll
-      for (int b = 2; b < 5; ++b) {                             // register bits 2-4 <-> row bits 0-2
-        const int hh = 1 << b;
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          if (i & hh) continue;
-          const double x = u[i], y = u[i + hh];
-          u[i] = x + y;
-          u[i + hh] = x - y;
-        }
+      for (int i = 0; i < 64; ++i) {
+        if (i & h) continue;
+        const double a = v[i], b = v[i + h];
+        v[i] = a + b;
+        v[i + h] = a - b;
       }
-#pragma unroll
-      for (int j = 0; j < 32; ++j) Epi<A2>::add(loc, u[j], al);
-    }
-#pragma unroll
-    for (int i = 0; i < NACC; ++i) acc[i] += loc[i];
+    tile_accumulate<A2>(acc, v, al);
+    if (al.hist) spec_add(shist, v);
   }
-  tmem_fence_before();
   block_flush(acc, partial, blockIdx.x);
-  if (w == 0) tmem_dealloc_warp(tbase, 512);
+  if (al.hist) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < SPEC_BINS; i += blockDim.x)
+      if (shist[i]) atomicAdd(al.hist + i, shist[i]);
+  }
 }
 
+// Per-call control block in the workspace (zeroed by the host before each range): a nonzero
+// error makes k_reduce write NaN sums.
+struct Ctl {
+  int error;
+};
 // ------------------------------------------------------------------------------------------
 // reduction of per-CTA partials (fixed order) + rescale t = 4 t' (DESIGN "Half-length").
 //   out[s*(n+2)+i] = scale_i * sum_slot partial[s][slot][i]

@@ -73,6 +73,24 @@ def test_two_pass_ranges_vs_oracle(sre, oracle_lib, n):
             assert abs(g[-1] - o[-1]) <= 1e-10 * abs(o[-1])
 
 
+@pytest.mark.parametrize("n", [21, 22, 23, 24])
+def test_streamed_production_batches_vs_oracle(sre, oracle_lib, n):
+    """N = 21..24 at the production launch size: a full K-aligned batch (K = 64 at N = 21, 32 above)
+    runs the radix-64 pass A (k_passAr, every group of 4 active) and the TMA pass B; a second range
+    ends mid-group (kcount = 8 m + 5: the last group of 4 has one active X-string) and a third covers
+    an a_h with a high pivot.  Raw sums vs the Alg. 2 oracle at 1e-10 for alpha = 1, 2, 3."""
+    psi = si.haar(n, 4100 + n)
+    K = 64 if n == 21 else 32
+    D = 1 << n
+    ranges = [(5 * K * 4096 // K * K, 5 * K * 4096 // K * K + K), (D // 2 + 8 * 1024, D // 2 + 8 * 1024 + 13),
+              (D - 2 * K, D - K)]
+    for lo, hi in ranges:
+        g = gpu_sums(sre, psi, [1.0, 2.0, 3.0], lo, hi)[0]
+        o = oracle_lib.sums_fwht(psi, [1.0, 2.0, 3.0], a_range=(lo, hi))
+        assert rel(g[:-1], o[:-1]) < 1e-10, (lo, hi)
+        assert abs(g[-1] - o[-1]) <= 1e-10 * abs(o[-1]), (lo, hi)
+
+
 @pytest.mark.parametrize("n", [1, 2, 5, 6, 10, 11, 13, 14, 15, 17, 20])
 def test_chi_elementwise(sre, oracle_lib, n):
     """chi_b(a) for every b, sampled a, element by element against the oracle's Alg. 2 transform."""
