@@ -65,6 +65,76 @@ def ncu_traffic(config, kind):
     return t["dram_bytes_per_launch"] if t and t.get("kind") == kind else None
 
 
+def two_pass_L(n):
+    """Low-bit count of pass A per N (csrc/sre_api.cu two_pass_params)."""
+    if n <= 20:
+        return 10
+    return 12 if n <= 24 else 13
+
+
+def epilogue_ops(alphas):
+    """FP64 ops per Pauli string of the power-sum epilogue: t = y^2 and the purity
+    add (2); alpha = 2 alone: 1 FMA; integer alpha: (alpha - 1) multiplies + 1 add; alpha = 1: the
+    logarithm (ln_fast: 9-term polynomial + division + scaling, ~26) + 1 FMA; non-integer alpha:
+    the shared logarithm + exp_fast (~20) + 2."""
+    ops = 2
+    if alphas == [2.0]:
+        return ops + 1
+    need_log = any(a == 1.0 for a in alphas)
+    real = [a for a in alphas if not (a == int(a) and 1 <= a <= 64)]
+    if need_log or real:
+        ops += 26
+    if need_log:
+        ops += 1
+    for a in alphas:
+        if a == 1.0:
+            continue
+        ops += (int(a) - 1 + 1) if a == int(a) else 22
+    return ops
+
+
+def roofline(n, b, alphas, dom, avg_ms, paulis_per_launch, peaks, peak_src, sm_mhz):
+    """roofline object of the bench line for the dominant kernel kind.
+    Two-pass N >= 15: HBM-bound -- pass A moves 8 B/Pauli of workspace writes plus one read of psi per
+    launch (2^N x 16 B: the launch's X-strings re-read each psi row from L2); pass B reads 8 B/Pauli.
+    Single pass N <= 14: no workspace; FP64-pipe bound (psi operands from L2).  Alongside: the FP64
+    fraction of the same kernel at the run's max SM clock."""
+    fp64_peak = FP64_OPS_PER_CLK_SM * 148 * sm_mhz * 1e6 / 1e12
+    L = two_pass_L(n)
+    if dom == "pass_a":
+        ops = 2 + L
+        bytes_launch = 8.0 * paulis_per_launch + 16.0 * (1 << n) * b
+    elif dom == "pass_b":
+        ops = (n - 1 - L) + epilogue_ops(alphas)
+        bytes_launch = 8.0 * paulis_per_launch
+    else:
+        ops = 2 + (n - 1) + epilogue_ops(alphas)
+        bytes_launch = None
+    fp64 = ops * paulis_per_launch / (avg_ms * 1e-3) / 1e12
+    fp64_obj = {"achieved": fp64, "peak": fp64_peak, "unit": "TFLOP/s (FP64 ops)", "frac": fp64 / fp64_peak,
+                "ops_per_pauli": ops,
+                "peak_source": f"64 FP64 ops/clk/SM x 148 SMs x {sm_mhz:.0f} MHz (guide unit count; measured 63.9)"}
+    if bytes_launch is not None:
+        gbs = bytes_launch / (avg_ms * 1e-3) / 1e9
+        return {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": gbs / peaks["hbm_gbs"], "traffic": None, "peak_source": peak_src,
+                "bytes_per_launch": bytes_launch, "bytes_per_pauli": bytes_launch / paulis_per_launch,
+                "fp64": fp64_obj}
+    return {"bound": "alu", "achieved": fp64, "peak": fp64_peak, "unit": "TFLOP/s (FP64 ops)",
+            "frac": fp64 / fp64_peak, "traffic": None, "peak_source": fp64_obj["peak_source"], "ops_per_pauli": ops}
+
+
+def ncu_limiter(config, kind):
+    """The measured limiter of the dominant kernel from its committed `ncu --set full` capture
+    (profiles/r02_limiters.json, written from the summaries in profiles/), else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_limiters.json")) as f:
+            t = json.load(f).get(config, {}).get(kind)
+    except (OSError, ValueError):
+        return None
+    return t
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -567,17 +637,21 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     label, n, b, alphas, seed = CONFIGS[args.config]
     D = 1 << n
-    from paper_2601_07824_b200.dist import shard_range
-    lo, hi = shard_range(n, rank, world)                 # contiguous X-string shard
+    from paper_2601_07824_b200.dist import shard_range, state_shard
+    by_state = b > 1 and b >= world and world > 1      # batched workload: whole states per rank
+    lo, hi = (0, D) if by_state else shard_range(n, rank, world)   # else a contiguous X-string shard
+    s0, s1 = state_shard(b, rank, world) if by_state else (0, b)
     psi_host = make_state(args.config)
     psi = torch.from_numpy(psi_host).to(dev)            # replicated on every GPU (same seed)
     ws = torch.empty(sre.workspace_size(n, b, len(alphas)), dtype=torch.uint8, device=dev)
-    sums = torch.empty((b, len(alphas) + 2), dtype=torch.float64, device=dev)
+    sums = torch.zeros((b, len(alphas) + 2), dtype=torch.float64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > L2 (126 MB)
     stream = torch.cuda.current_stream(dev)
+    mine = psi[s0:s1] if b > 1 else psi
 
     def step():
-        sre.partial_sums(psi, lo, hi, alphas, out=sums, workspace=ws, stream=stream)
+        if s1 > s0:
+            sre.partial_sums(mine, lo, hi, alphas, out=sums[s0:s1], workspace=ws, stream=stream)
         if world > 1:
             dist.all_reduce(sums)                        # the one exchange step (NCCL, NVLink)
         return sre.finalize(sums, n, alphas)             # D2H of (n_alpha+2) doubles per state
@@ -612,6 +686,7 @@ def main():
         dist.barrier()
     paulis_per_step = float(b) * 4.0 ** n
     value = args.steps * paulis_per_step / (tot_ms * 1e-3)
+    rank_paulis_per_step = float(s1 - s0) * 4.0 ** n * (hi - lo) / D   # this rank's share
 
     # ---- end-to-end through the public C entry with host (pinned) buffers, N=1 semantics per rank
     e2e = None
@@ -635,54 +710,28 @@ def main():
         return 0
 
     peaks, peak_src = load_peaks()
-    # dominant kernel and its roofline
     kinds = {k: v for k, v in prof.items() if v["timed"] > 0 and k != "aux"}
     share = {k: v["ms_sum"] / v["timed"] * v["launched"] for k, v in kinds.items()}
     dom = max(share, key=share.get)
     avg_ms = prof[dom]["ms_sum"] / prof[dom]["timed"]
     launched = prof[dom]["launched"]
-    paulis_per_launch = paulis_per_step * args.steps / max(1, world) / launched
-    nq = n
-    # FP64 ops per Pauli string per kernel kind
-    ops = {"single_pass": 2 + (nq - 1) + 3, "pass_a": 2 + 0, "pass_b": 3}
-    if dom == "pass_a":
-        L = {15: 10, 16: 10, 17: 10, 18: 10, 19: 10, 20: 10, 21: 11, 22: 12, 23: 13}.get(nq, 13)
-        ops_unit = 2 + L
-        bytes_unit = 8 + 16.0 / 1.0   # workspace write + psi reads (two complex per 2 outputs)
-    elif dom == "pass_b":
-        L = {15: 10, 16: 10, 17: 10, 18: 10, 19: 10, 20: 10, 21: 11, 22: 12, 23: 13}.get(nq, 13)
-        ops_unit = (nq - 1 - L) + 3
-        bytes_unit = 8.0
-    else:
-        ops_unit = ops["single_pass"]
-        bytes_unit = 16.0
+    paulis_per_launch = rank_paulis_per_step * args.steps / launched
     sm_mhz = (clk or {}).get("sm_max_mhz", peaks.get("sm_max_mhz", 1965.0))
-    if n >= 23:
-        peak = peaks["hbm_gbs"]
-        achieved = bytes_unit * paulis_per_launch / (avg_ms * 1e-3) / 1e9
-        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": None, "peak_source": peak_src}
-    else:
-        peak = FP64_OPS_PER_CLK_SM * 148 * sm_mhz * 1e6 / 1e12
-        achieved = ops_unit * paulis_per_launch / (avg_ms * 1e-3) / 1e12
-        roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s (FP64 ops)",
-                "frac": achieved / peak, "traffic": None,
-                "peak_source": f"64 FP64 ops/clk/SM x 148 SMs x {sm_mhz:.0f} MHz (guide unit count; measured 63.9)"}
+    roof = roofline(n, b, alphas, dom, avg_ms, paulis_per_launch, peaks, peak_src, sm_mhz)
     roof["traffic"] = ncu_traffic(args.config, dom)
     roof.update({"kernel": dom, "avg_launch_ms": avg_ms, "launches_timed": prof[dom]["timed"],
-                 "share_of_step": share[dom] / tot_ms if world == 1 else None,
-                 "ops_per_pauli": ops_unit, "bytes_per_pauli": bytes_unit})
-    if n <= 20:
-        roof["limiter"] = {"resource": "L1TEX data pipe (LDS/STS/SHFL/LDG/STG share it)",
-                           "pct_of_peak": "79-88 (ncu, k_passA10s)",
-                           "source": "profiles/r01_ncu_summary_n20_v3.txt; DESIGN.md section 6"}
+                 "share_of_step": share[dom] / tot_ms if world == 1 else None})
+    lim = ncu_limiter(args.config, dom)
+    if lim:
+        roof["limiter"] = lim
     hbm_equiv = 16.0 * value / max(1, world) / 1e9      # FWHT workspace bytes per Pauli string (16 B)
     line = {
         "metric": METRIC, "value": value, "unit": "Pauli strings/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": label, "N": n, "batch": b, "alphas": alphas, "seed": seed,
-                   "x_string_shards": world, "l2": "flushed between steps (256 MiB write)",
+                   "shards": f"{world} state shards" if by_state else f"{world} X-string shards",
+                   "l2": "flushed between steps (256 MiB write)",
                    "step": "partial_sums over all 2^N X-strings + allreduce + finalize"},
         "roofline": roof,
         "fwht_hbm_equiv": {"GBps_per_gpu": hbm_equiv, "frac_of_hbm": hbm_equiv / peaks["hbm_gbs"],

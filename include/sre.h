@@ -147,8 +147,12 @@ int sre_norm2(const void* psi, int N, int B, double* out_dev, void* stream);
 
 /*
  * sre_chi -- debug/verification entry: chi_b(a) = <psi|X_a Z_b|psi> for one X-string a and all
- * b (Eq. (12)), computed by the same kernels as the sums, written to device chi_dev[2*2^N]
- * as complex128 in natural b order (each chi is purely real or purely imaginary, DESIGN C3).
+ * b (Eq. (12)), computed by the kernels that evaluate that X-string in the sums -- the single-pass
+ * kernels for N <= 14; for N >= 15 the production staged (N <= 20) or streamed (N = 21..24) pass A
+ * and TMA pass B when a >= 2^L and a % 8 == 0 (their pass-B epilogue decodes every output), else
+ * the generic two-pass kernels that take such head X-strings in the sums -- written to device
+ * chi_dev[2*2^N] as complex128 in natural b order (each chi is purely real or purely imaginary,
+ * DESIGN C3).  Synchronous on `stream`.
  */
 int sre_chi(const void* psi, int N, uint64_t a, double* chi_dev, void* stream);
 

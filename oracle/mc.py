@@ -61,10 +61,12 @@ def mean_f_exact(f: np.ndarray, beta: float) -> float:
 
 
 def ti_exact(psi, L: int, epsilon: float = 0.0) -> float:
+    """M_2 = -log2(e^{-I} - eps), I = sum_l w_l <f>_l: Eq. (M2_TI_reg_explicit_correct)
+    written in reading C16's sign (I = ln Z_0 - ln Z_1, Z_0 = 2^N, Z_1 = S_2 + 2^N eps); = I / ln 2 at eps = 0."""
     f = all_energies(psi, epsilon)
     betas, w = simpson(L)
     integral = sum(wl * mean_f_exact(f, b) for b, wl in zip(betas, w))
-    return integral / math.log(2.0)     # M_2 = +I / ln 2 (reading C16)
+    return -math.log2(math.exp(-integral) - epsilon)
 
 
 def mc_replay(psi, L: int, streams, burn_in: int, n_samples: int, epsilon: float = 0.0):

@@ -117,6 +117,21 @@ def _psi_ptr(psi):
     return a.ctypes.data, _nqubits(a.shape[-1]), b, a
 
 
+def _bind_stream(st, psi, keep, *tensors):
+    """Make the tensors a call enqueues on ``st`` safe when ``st`` is not torch's current stream: a
+    contiguous copy of psi (made on the current stream) is waited for, and every tensor the kernels use
+    is recorded on ``st`` so the caching allocator cannot recycle it before they finish."""
+    import torch
+    cur = torch.cuda.current_stream(st.device)
+    if st == cur:
+        return
+    if keep is not psi:
+        st.wait_stream(cur)
+    for t in (keep,) + tensors:
+        if isinstance(t, torch.Tensor) and t.is_cuda:
+            t.record_stream(st)
+
+
 def _prec(precision: str) -> int:
     if precision not in PRECISION:
         raise SreError(1, f"precision {precision!r}: one of {sorted(PRECISION)}")
@@ -125,6 +140,7 @@ def _prec(precision: str) -> int:
 
 def exact(psi, alphas: Sequence[float] = (2.0,), precision: str = "fp64"):
     """M_alpha (bits) and lost_norm of one state -- Eq. (2) via Alg. 2 over all 2^N X-strings.
+    Synchronous; runs on the legacy default stream (which waits for torch's blocking streams).
     psi: complex128 torch tensor (cuda: no copy; cpu) or numpy array (host: copied by the call).
     precision "fp32" selects the optional FP32 transform (FP64 accumulation, ~1e-4 relative)."""
     lib = load()
@@ -176,6 +192,7 @@ def partial_sums(psi, a_begin: int, a_end: int, alphas: Sequence[float], out=Non
     if workspace is None or workspace.numel() < ws_need:
         workspace = torch.empty(ws_need, dtype=torch.uint8, device=dev)
     st = stream if stream is not None else torch.cuda.current_stream(dev)
+    _bind_stream(st, psi, keep, out, workspace)
     _check(lib.sre_partial_sums_ex(ctypes.c_void_p(ptr), n, b, int(a_begin), int(a_end), _dp(al), al.size,
                                    _prec(precision), ctypes.c_void_p(workspace.data_ptr()), workspace.numel(),
                                    ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(st.cuda_stream)))
@@ -201,6 +218,7 @@ def x_string_sums(psi, a_list, alphas: Sequence[float] = (2.0,), out=None, works
     if workspace is None or workspace.numel() < ws_need:
         workspace = torch.empty(ws_need, dtype=torch.uint8, device=psi.device)
     st = stream if stream is not None else torch.cuda.current_stream(psi.device)
+    _bind_stream(st, psi, keep, out, workspace)
     _check(lib.sre_x_string_sums(ctypes.c_void_p(ptr), n, a.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
                                  a.size, _dp(al), al.size, ctypes.c_void_p(workspace.data_ptr()), workspace.numel(),
                                  ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(st.cuda_stream)))
@@ -264,9 +282,11 @@ def spectrum(psi, a_begin: int = 0, a_end: int | None = None, workspace=None, st
     if workspace is None or workspace.numel() < ws_need:
         workspace = torch.empty(ws_need, dtype=torch.uint8, device=psi.device)
     st = stream if stream is not None else torch.cuda.current_stream(psi.device)
+    _bind_stream(st, psi, keep, hist, workspace)
     _check(lib.sre_pauli_spectrum(ctypes.c_void_p(ptr), n, int(a_begin), int(a_end), ctypes.c_void_p(hist.data_ptr()),
                                   ctypes.c_void_p(workspace.data_ptr()), workspace.numel(),
                                   ctypes.c_void_p(st.cuda_stream)))
+    st.synchronize()                                  # the histogram is complete on st before the copy
     del keep
     return hist.cpu().numpy()
 

@@ -101,16 +101,27 @@ template <class K>
 cudaError_t set_smem(K kern, int bytes) {
   return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
+// Raise a kernel's dynamic shared-memory limit once per device (bit d of `mask`): the attribute is per
+// device context, so a process that switches devices must set it again there.
+template <class K>
+cudaError_t set_smem_once(K kern, int bytes, uint64_t& mask) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 64 && ((mask >> dev) & 1ull)) return cudaSuccess;
+  e = set_smem(kern, bytes);
+  if (e == cudaSuccess && dev < 64) mask |= 1ull << dev;
+  return e;
+}
 
 template <class V, int T, bool A2, bool DBG>
 cudaError_t launch_mid_t(const typename Cx<V>::T* psi, int N, int B, int gx, uint64_t a0, uint64_t count, const Alphas& al,
                          double* partial, double* chi, cudaStream_t st, const uint64_t* alist,
                            unsigned long long* hist = nullptr) {
-  static bool init = false;
-  if (!init) {
-    cudaError_t e = set_smem(k_mid<T, A2, DBG, V>, SMEM_128K);
+  static uint64_t init_mask = 0;   // per device: the attribute belongs to the device context
+  {
+    cudaError_t e = set_smem_once(k_mid<T, A2, DBG, V>, SMEM_128K, init_mask);
     if (e != cudaSuccess) return e;
-    init = true;
   }
   dim3 grid(gx, B);
   return launch_counted(LK_SINGLE, st, [&] {
@@ -133,11 +144,10 @@ cudaError_t launch_mid(int T, const typename Cx<V>::T* psi, int N, int B, int gx
 
 template <class V, int L>
 cudaError_t launch_passA_t(const typename Cx<V>::T* psi, int N, uint64_t a0, int kcount, V* ws, int units, cudaStream_t st) {
-  static bool init = false;
-  if (!init) {
-    cudaError_t e = set_smem(k_passA<L, V>, SMEM_128K);
+  static uint64_t init_mask = 0;   // per device: the attribute belongs to the device context
+  {
+    cudaError_t e = set_smem_once(k_passA<L, V>, SMEM_128K, init_mask);
     if (e != cudaSuccess) return e;
-    init = true;
   }
   const uint64_t items = (uint64_t)kcount << (N - 1 - L);
   const unsigned grid = (unsigned)((items + units - 1) / units);
@@ -163,11 +173,10 @@ cudaError_t launch_passB_t(const Plan& p, uint64_t a0, int kcount, const V* ws, 
                            double* chi, cudaStream_t st) {
   constexpr int BLK = TP >= 14 ? 512 : 256;
   constexpr int SM = padded(BLK * 32) * 8;
-  static bool init = false;
-  if (!init) {
-    cudaError_t e = set_smem(k_passB<TP, CB, A2, DBG, V>, SM);
+  static uint64_t init_mask = 0;   // per device: the attribute belongs to the device context
+  {
+    cudaError_t e = set_smem_once(k_passB<TP, CB, A2, DBG, V>, SM, init_mask);
     if (e != cudaSuccess) return e;
-    init = true;
   }
   const uint64_t items = (uint64_t)kcount * 2 * (1ull << (p.L - CB));
   const unsigned grid = (unsigned)((items + p.unitsB - 1) / p.unitsB);
@@ -192,11 +201,10 @@ cudaError_t launch_passB(const Plan& p, uint64_t a0, int kcount, const V* ws, co
 template <class V, int N>
 cudaError_t launch_passA10s_t(const Dev& d, const typename Cx<V>::T* psi, uint64_t a_first, int kcount, V* ws,
                               cudaStream_t st) {
-  static bool init = false;
-  if (!init) {
-    cudaError_t e = set_smem(k_passA10s<N, V>, PA10_SMEM);
+  static uint64_t init_mask = 0;   // per device: the attribute belongs to the device context
+  {
+    cudaError_t e = set_smem_once(k_passA10s<N, V>, PA10_SMEM, init_mask);
     if (e != cudaSuccess) return e;
-    init = true;
   }
   const int groups = (kcount + 7) / 8;
   const uint64_t items = (uint64_t)groups << (N - 11);
@@ -210,11 +218,10 @@ cudaError_t launch_passA10s_t(const Dev& d, const typename Cx<V>::T* psi, uint64
 template <class V, int N, int L>
 cudaError_t launch_passAs_t(const Dev& d, const typename Cx<V>::T* psi, uint64_t a_first, int kcount, V* ws,
                             cudaStream_t st) {
-  static bool init = false;
-  if (!init) {
-    cudaError_t e = set_smem(k_passAs<N, L, V>, pas_smem(L));
+  static uint64_t init_mask = 0;   // per device: the attribute belongs to the device context
+  {
+    cudaError_t e = set_smem_once(k_passAs<N, L, V>, pas_smem(L), init_mask);
     if (e != cudaSuccess) return e;
-    init = true;
   }
   const uint64_t units = (uint64_t)kcount << (N - 1 - L);
   const uint64_t ctas = (units + (256 >> (L - 5)) - 1) / (256 >> (L - 5));
@@ -227,16 +234,16 @@ cudaError_t launch_passAs_t(const Dev& d, const typename Cx<V>::T* psi, uint64_t
 
 template <int N>
 cudaError_t launch_passAr_t(const Dev& d, const double2* psi, uint64_t a_first, int kcount, double* ws, cudaStream_t st) {
-  static bool init = false;
-  if (!init) {
-    cudaError_t e = set_smem(k_passAq<N>, PAQ_SMEM);
+  static uint64_t init_mask = 0;   // per device: the attribute belongs to the device context
+  {
+    cudaError_t e = set_smem_once(k_passAq<N>, PAQ_SMEM, init_mask);
     if (e != cudaSuccess) return e;
-    init = true;
   }
   const uint64_t items = (uint64_t)kcount << (N - 15);               // (4-row block, X-string)
   const unsigned grid = (unsigned)(items < (uint64_t)d.sms ? items : (uint64_t)d.sms);
+  const uint64_t kmagic = ((1ull << 40) + (uint64_t)kcount - 1) / (uint64_t)kcount;
   return launch_counted(LK_PASSA, st, [&] {
-    k_passAq<N><<<grid, 256, PAQ_SMEM, st>>>(psi, a_first, kcount, ws);
+    k_passAq<N><<<grid, 256, PAQ_SMEM, st>>>(psi, a_first, kcount, kmagic, ws);
     return cudaGetLastError();
   });
 }
@@ -273,11 +280,10 @@ cudaError_t launch_passA10s(const Plan& p, const Dev& d, const typename Cx<V>::T
 template <class V, int TP, int CB, bool A2>
 cudaError_t launch_passBt_t(const Plan& p, const Dev& d, int kcount, const V* ws, const Alphas& al,
                             double* partial, cudaStream_t st) {
-  static bool init = false;
-  if (!init) {
-    cudaError_t e = set_smem(k_passBt<TP, CB, A2, V>, pbt_smem(TP));
+  static uint64_t init_mask = 0;   // per device: the attribute belongs to the device context
+  {
+    cudaError_t e = set_smem_once(k_passBt<TP, CB, A2, V>, pbt_smem(TP), init_mask);
     if (e != cudaSuccess) return e;
-    init = true;
   }
   const unsigned grid = (unsigned)d.sms;
   return launch_counted(LK_PASSB, st, [&] {
@@ -286,17 +292,16 @@ cudaError_t launch_passBt_t(const Plan& p, const Dev& d, int kcount, const V* ws
   });
 }
 
-template <int CB, bool A2>
+template <int CB, int L, bool A2>
 cudaError_t launch_passBr_t(const Dev& d, int kcount, const double* ws, const Alphas& al, double* partial,
                             cudaStream_t st) {
-  static bool init = false;
-  if (!init) {
-    cudaError_t e = set_smem(k_passBr<CB, A2>, PBR_SMEM);
+  static uint64_t init_mask = 0;   // per device: the attribute belongs to the device context
+  {
+    cudaError_t e = set_smem_once(k_passBr<CB, L, A2>, PBR_SMEM, init_mask);
     if (e != cudaSuccess) return e;
-    init = true;
   }
   return launch_counted(LK_PASSB, st, [&] {
-    k_passBr<CB, A2><<<d.sms, 256, PBR_SMEM, st>>>(kcount, ws, al, partial);
+    k_passBr<CB, L, A2><<<d.sms, 256, PBR_SMEM, st>>>(kcount, ws, al, partial);
     return cudaGetLastError();
   });
 }
@@ -307,10 +312,18 @@ cudaError_t launch_passBp(const Plan& p, const Dev& d, int kcount, const V* ws, 
   if constexpr (std::is_same<V, double>::value) {   // FP64 N = 21..24: radix-64 pass B (one transpose)
     if (p.N >= 21 && p.N <= 24 && !p.legacyB) {
       switch (13 - p.H) {
-        case 5: return launch_passBr_t<5, A2>(d, kcount, ws, al, partial, st);
-        case 4: return launch_passBr_t<4, A2>(d, kcount, ws, al, partial, st);
-        case 3: return launch_passBr_t<3, A2>(d, kcount, ws, al, partial, st);
-        case 2: return launch_passBr_t<2, A2>(d, kcount, ws, al, partial, st);
+        case 5: return launch_passBr_t<5, 12, A2>(d, kcount, ws, al, partial, st);
+        case 4: return launch_passBr_t<4, 12, A2>(d, kcount, ws, al, partial, st);
+        case 3: return launch_passBr_t<3, 12, A2>(d, kcount, ws, al, partial, st);
+        case 2: return launch_passBr_t<2, 12, A2>(d, kcount, ws, al, partial, st);
+      }
+    }
+    if (p.N >= 17 && p.N <= 20) {   // k_passA10s wrote 2^13-double tiles for these (its cb = 13 - H)
+      switch (13 - p.H) {
+        case 7: return launch_passBr_t<7, 10, A2>(d, kcount, ws, al, partial, st);
+        case 6: return launch_passBr_t<6, 10, A2>(d, kcount, ws, al, partial, st);
+        case 5: return launch_passBr_t<5, 10, A2>(d, kcount, ws, al, partial, st);
+        case 4: return launch_passBr_t<4, 10, A2>(d, kcount, ws, al, partial, st);
       }
     }
   }

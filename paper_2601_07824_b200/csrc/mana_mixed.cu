@@ -345,15 +345,17 @@ LegFn leg_fn(int sp, int nl, bool fin, int threads) {
 
 int occupancy(const void* fn, size_t smem, int threads) {
   static std::mutex mu;
-  static std::vector<std::pair<const void*, int>> seen;
+  static std::vector<std::pair<std::pair<const void*, int>, int>> seen;   // (kernel, device) -> CTAs per SM
   std::lock_guard<std::mutex> lk(mu);
+  int dev = 0;
+  cudaGetDevice(&dev);                          // the smem attribute is per device context
   for (auto& s : seen)
-    if (s.first == fn) return s.second;
+    if (s.first.first == fn && s.first.second == dev) return s.second;
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem) != cudaSuccess || occ < 1) occ = 1;
   cudaGetLastError();
-  seen.push_back({fn, occ});
+  seen.push_back({{fn, dev}, occ});
   return occ;
 }
 

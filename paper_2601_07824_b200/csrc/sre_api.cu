@@ -424,15 +424,14 @@ int run_list(const double2* psi, int N, const uint64_t* alist_dev, int n_a, cons
 }
 
 // internal cached device buffers for the synchronous calls
-struct Cache {
-  std::mutex mu;
+struct Cache {                 // one per device: buffers stay with the device that allocated them
   char* ws = nullptr;
   size_t ws_bytes = 0;
   char* in = nullptr;
   size_t in_bytes = 0;
-  int dev = -1;
 };
-Cache g_cache;
+std::mutex g_cache_mu;
+Cache g_caches[64];
 
 int cache_get(char** buf, size_t* have, size_t need) {
   if (*have >= need) return SRE_OK;
@@ -459,10 +458,8 @@ int exact_impl(const void* psi, int N, int B, const double* alpha, int n_alpha, 
   if (rc) return rc;
   bool dev_ptr = false;
   is_device_ptr(psi, dev_ptr);
-  std::lock_guard<std::mutex> lk(g_cache.mu);
-  if (g_cache.dev != d.id) {  // device switched: drop cached buffers of the old device
-    g_cache.ws = nullptr; g_cache.ws_bytes = 0; g_cache.in = nullptr; g_cache.in_bytes = 0; g_cache.dev = d.id;
-  }
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  Cache& g_cache = g_caches[d.id];
   Plan p;
   make_plan(N, d, p);
   const size_t need = ws_bytes_for(p, B, prec) + sizeof(double) * ((size_t)B * (n_alpha + 2) + (size_t)B);
@@ -693,13 +690,23 @@ int sre_chi(const void* psi, int N, uint64_t a, double* chi_dev, void* stream) {
   } else if (p.kind == MID) {
     e = launch_mid<double, false, true>(p.T, dpsi, N, 1, 1, a, 1, al, nullptr, chi_dev, st, nullptr);
   } else {
-    std::lock_guard<std::mutex> lk(g_cache.mu);
-    if (g_cache.dev != d.id) { g_cache.ws = nullptr; g_cache.ws_bytes = 0; g_cache.in = nullptr; g_cache.in_bytes = 0; g_cache.dev = d.id; }
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    Cache& g_cache = g_caches[d.id];
     rc = cache_get(&g_cache.ws, &g_cache.ws_bytes, ws_bytes_for(p, 1));
     if (rc) return rc;
     double* slab = reinterpret_cast<double*>(g_cache.ws + off_slab(p, 1));
-    e = launch_passA<double>(p, dpsi, a, 1, slab, st);
-    if (e == cudaSuccess) e = launch_passB<double, false, true>(p, a, 1, slab, al, nullptr, chi_dev, st);
+    if (p.staged && a >= p.amin && a % 8 == 0) {
+      // the production kernels of the sums (staged / streamed pass A + TMA pass B, kcount = 1): the pass-B
+      // epilogue decodes every output into chi_b(a) (Alphas::chi); its sums land in scratch slots
+      double* partial = reinterpret_cast<double*>(g_cache.ws);
+      al.chi = chi_dev;
+      al.chi_a0 = a;
+      e = launch_passA10s<double>(p, d, dpsi, a, 1, slab, st);
+      if (e == cudaSuccess) e = launch_passBp<double, false>(p, d, 1, slab, al, partial, st);
+    } else {   // generic head (a < 2^L or unaligned): the kernels those X-strings take in the sums
+      e = launch_passA<double>(p, dpsi, a, 1, slab, st);
+      if (e == cudaSuccess) e = launch_passB<double, false, true>(p, a, 1, slab, al, nullptr, chi_dev, st);
+    }
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   }
   if (e != cudaSuccess) return fail(SRE_ECUDA, "sre_chi: %s", cudaGetErrorString(e));

@@ -33,6 +33,8 @@ struct Alphas {
   int need_log;         // any alpha == 1
   int any_real;         // any kind == 2 (non-integer alpha)
   unsigned long long* hist;   // spectrum epilogue (two-pass kernels; nullptr = off)
+  double* chi;          // sre_chi through the production pass-B kernels: chi_b(a) element-wise (nullptr = off)
+  unsigned long long chi_a0;  // first X-string of the launch (chi mode)
   int kind[MAXA];       // 0: integer exponent iexp[i] >= 1, 2: general real power
   int iexp[MAXA];
   double alpha[MAXA];
@@ -171,42 +173,83 @@ struct Epi {
   }
 };
 
-// Epilogue of one tile's 32 values per thread into a fresh local sum, then one add into the
-// long-lived accumulators: keeps the running-sum chains ~32x shorter (DESIGN "Summation").
-// General alphas run in three compact phases (integer powers + purity; t ln t if some alpha = 1;
-// real powers if some alpha is non-integer): interleaving the rarely-taken exp/log blocks with
-// the common path made the executed code sparse in a ~200 KB body (10x slower, I-cache bound).
+// Natural logarithm for the general-alpha epilogue (t > 0 normal):
+// t = 2^e m with m in [sqrt(1/2), sqrt(2)), ln t = e ln 2 + 2 atanh(s), s = (m - 1)/(m + 1), |s| <= 0.1716,
+// 2 atanh(s) = 2 s (1 + s^2/3 + ... + s^18/19): truncation s^20/21 < 1e-17 relative, so the result is
+// within a few ulp (the CUDA log() spends ~4x the instructions on correct rounding we do not need:
+// every term of sum t ln t has the same sign, so 1e-15 relative per term is far inside the 1e-10 bar).
+__device__ __forceinline__ double ln_fast(double t) {
+  long long b = __double_as_longlong(t);
+  int e = (int)((b >> 52) & 0x7ff) - 1023;
+  double m = __longlong_as_double((b & 0x000fffffffffffffLL) | 0x3ff0000000000000LL);   // [1, 2)
+  const bool hi = m > 1.4142135623730951;
+  m = hi ? 0.5 * m : m;
+  e += hi ? 1 : 0;
+  const double s = (m - 1.0) / (m + 1.0);
+  const double s2 = s * s;
+  double p = 1.0 / 19;
+  p = fma(p, s2, 1.0 / 17); p = fma(p, s2, 1.0 / 15); p = fma(p, s2, 1.0 / 13); p = fma(p, s2, 1.0 / 11);
+  p = fma(p, s2, 1.0 / 9); p = fma(p, s2, 1.0 / 7); p = fma(p, s2, 1.0 / 5); p = fma(p, s2, 1.0 / 3);
+  const double ls = fma(2.0 * s * s2, p, 2.0 * s);                                        // 2 atanh(s)
+  return fma((double)e, 0.6931471805599453, fma((double)e, 2.3190468138462996e-17, ls)); // e ln2 (hi + lo)
+}
+// e^z for z <= 0 (t^alpha = e^(alpha ln t)): z = k ln 2 + r, |r| <= ln2/2, Taylor to r^13
+// (truncation r^14/14! < 2e-17 relative); 2^k applied in two exponent steps; z < -745 -> 0.
+__device__ __forceinline__ double exp_fast(double z) {
+  if (!(z > -745.0)) return 0.0;
+  const double k = rint(z * 1.4426950408889634);
+  const double r = fma(-k, 2.3190468138462996e-17, fma(-k, 0.6931471805599453, z));
+  double p = 1.0 / 6227020800.0;
+  p = fma(p, r, 1.0 / 479001600.0); p = fma(p, r, 1.0 / 39916800.0); p = fma(p, r, 1.0 / 3628800.0);
+  p = fma(p, r, 1.0 / 362880.0); p = fma(p, r, 1.0 / 40320.0); p = fma(p, r, 1.0 / 5040.0);
+  p = fma(p, r, 1.0 / 720.0); p = fma(p, r, 1.0 / 120.0); p = fma(p, r, 1.0 / 24.0);
+  p = fma(p, r, 1.0 / 6.0); p = fma(p, r, 0.5); p = fma(p, r, 1.0); p = fma(p, r, 1.0);
+  const int ki = (int)k;                                                                // in [-1075, 1]
+  const int k1 = ki / 2, k2 = ki - k1;
+  return p * __longlong_as_double((long long)(k1 + 1023) << 52) * __longlong_as_double((long long)(k2 + 1023) << 52);
+}
+__device__ __forceinline__ float ln_fast(float t) { return logf(t); }
+__device__ __forceinline__ float exp_fast(float z) { return expf(z); }
+
+// Epilogue of one tile's values per thread into a fresh local sum, then one add into the long-lived
+// accumulators: keeps the running-sum chains short (DESIGN "Summation").  General alphas run in
+// compact phases (integer powers + purity; t ln t if some alpha = 1; real powers if some alpha is
+// non-integer), four values per step of a rolled loop: unrolling a full tile of log/exp bodies made
+// the kernel instruction-cache bound in round 1.  Terms with t below 1e-300 add 0 (t ln t > -1e-297).
 template <bool A2, class R, int M>
 __device__ __forceinline__ void tile_accumulate(double (&acc)[NACC], const R (&v)[M], const Alphas& al) {
-  R loc[NACC];          // FP32 mode: 32-term local sums in FP32, one conversion per tile
+  R loc[NACC];          // FP32 mode: local sums in FP32, one conversion per tile
 #pragma unroll
   for (int i = 0; i < NACC; ++i) loc[i] = R(0);
   if constexpr (A2) {
 #pragma unroll
     for (int j = 0; j < M; ++j) Epi<true, R>::add(loc, v[j], al);
   } else {
-    // General alphas: one compact (not unrolled) loop over the tile, t values staged through a
-    // per-thread local array (L1).  Unrolling 32 copies of log / exp(a log t) made the kernel
-    // instruction-cache bound (ncu: "no_instruction" the top stall).
     R tv[M];
 #pragma unroll
     for (int j = 0; j < M; ++j) tv[j] = v[j] * v[j];
 #pragma unroll 1
-    for (int j = 0; j < M; ++j) {
-      const R t = tv[j];
-      loc[MAXA] += t;
+    for (int j0 = 0; j0 < M; j0 += 4) {
 #pragma unroll
-      for (int i = 0; i < MAXA; ++i) {
-        if (i >= al.n) break;
-        if (al.kind[i] == 0) {
-          R pw = t;
-          for (int k = 1; k < al.iexp[i]; ++k) pw *= t;
-          loc[i] += pw;
-        } else {
-          loc[i] += (t > R(0)) ? exp(R(al.alpha[i]) * log(t)) : R(0);
+      for (int jj = 0; jj < 4; ++jj) {
+        const R t = tv[j0 + jj];
+        loc[MAXA] += t;
+        const bool pos = t > R(1e-300);
+        R lt = R(0);
+        if (al.need_log | al.any_real) lt = ln_fast(pos ? t : R(1));
+        if (al.need_log) loc[MAXA + 1] = fma(t, pos ? lt : R(0), loc[MAXA + 1]);
+#pragma unroll
+        for (int i = 0; i < MAXA; ++i) {
+          if (i >= al.n) break;
+          if (al.kind[i] == 0) {
+            R pw = t;
+            for (int k = 1; k < al.iexp[i]; ++k) pw *= t;
+            loc[i] += pw;
+          } else {
+            loc[i] += pos ? exp_fast(R(al.alpha[i]) * lt) : R(0);
+          }
         }
       }
-      if (al.need_log) loc[MAXA + 1] += (t > R(0)) ? t * log(t) : R(0);
     }
   }
 #pragma unroll
@@ -640,7 +683,9 @@ template <int N, class V = double>
 __global__ void __launch_bounds__(256, 1) k_passA10s(const typename Cx<V>::T* __restrict__ psi, uint64_t a_first,
                                                      int kcount, int groups, V* __restrict__ ws) {
   using C2 = typename Cx<V>::T;
-  constexpr int cb = 12 - (N - 11);                             // pass B tile = 2^12 values
+  // pass-B tile: 2^13 values for the FP64 radix-64 k_passBr (N = 17..20: 128-B or longer row runs),
+  // 2^12 for k_passBt (N = 15, 16 and the FP32 mode)
+  constexpr int cb = (std::is_same<V, double>::value && N >= 17 ? 13 : 12) - (N - 11);
   extern __shared__ __align__(128) double smem[];
   C2* ring = reinterpret_cast<C2*>(smem);                       // [NS][q row | r row][1024]
   V* exch = reinterpret_cast<V*>(smem + PA10_NS * 2 * 1024 * 2);   // [warp][padded 1024]
@@ -779,6 +824,21 @@ __global__ void __launch_bounds__(256, 1) k_passBt(int N, int kcount, const V* _
     tile_accumulate<A2>(acc, v[0], al);
     if constexpr (std::is_same<V, double>::value) {
       if (al.hist) spec_add(shist, v[0]);
+      if (al.chi) {   // sre_chi: element (row, col) of tile (k, plane, slab) is the output b' = (row << L) | b_l
+        constexpr int sf = final_s<TP, CB>();
+        const int L = N - 1 - (TP - CB);
+        const uint64_t kp = tile / slabs, slab = tile % slabs;
+        const uint64_t a = al.chi_a0 + (kp >> 1);
+        const int p = pivot_of(a, N);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const uint32_t e = lay(t, j, sf);
+          const uint64_t pos = (slab << CB) | (e & ((1u << CB) - 1u));
+          // k_passA10s stores frequency b_l = 32 lane + j at pos = lane + 32 j (N <= 20)
+          const uint64_t bl = L == 10 ? (((pos & 31) << 5) | (pos >> 5)) : pos;
+          chi_store(al.chi, a, p, (int)(kp & 1), ((uint64_t)(e >> CB) << L) | bl, v[0][j]);
+        }
+      }
     }
   }
   block_flush(acc, partial, blockIdx.x);
@@ -953,18 +1013,20 @@ __device__ __forceinline__ void bfly64(double (&v)[64]) {
 // register rounds and ONE shared-memory transpose (k_passAs: 32 values per thread, three rounds).
 //   CTA = 4 units (256 threads); an item is (block of 4 consecutive rows 4m..4m+3, X-string k);
 //   unit u transforms row 4m + u.  Each unit streams its two psi rows (x_h = ins0(y_h, p - 12) and
-//   x_h ^ a_h) in 16 chunks of 256 complex (q chunk c, r chunk c ^ (a_l >> 8): 8 KB per stage) through
-//   its own 3-deep bulk-copy ring.  Generation computes both planes; plane A stays in registers,
-//   plane B is parked in TMEM (128 columns per thread) until plane A is stored.
+//   x_h ^ a_h) in 16 chunks of 256 complex (q chunk c, r chunk c ^ (a_l >> 8): 8 KB per stage)
+//   through its own 3-deep bulk-copy ring.  Generation computes both planes; plane A stays in
+//   registers, plane B is parked in TMEM (128 columns per thread) until plane A is stored.
 //   Round 0: register index j = pos bits 6..11 (pos = t + 64 j).  Transpose through the unit's
 //   32 KB XOR-swizzled buffer (physical = e ^ ((e >> 6) & 15): conflict-free both ways, no pad).
-//   Round 1: j = pos bits 0..5 (pos = 64 t + j).
-//   Store: the 4 rows are staged in the CTA's 128 KB (the four transpose buffers) in workspace
-//   order -- per slab of 2^CB columns, rows 4m..4m+3 are contiguous in the slab-major workspace of
-//   k_passBt<13, CB = 13 - H>, i.e. 4 x 2^CB x 8 B (>= one 128-B line) per slab -- and written
-//   back with coalesced 16-B stores, every warp instruction covering whole lines.  Measured on B200
-//   (tools/microbench_wr.cu, N = 24): 32-B runs written one row at a time reach 1.9-2.2 TB/s of
-//   HBM, whole 4-row lines 4.5 TB/s.
+//   Round 1: j = pos bits 0..5 (pos = 64 t + j); each thread writes 16 runs of 4 doubles into the
+//   slab-major workspace of k_passBr<CB = 13 - H> with 32-byte stores.
+// Why 4 rows of one X-string per CTA: at N = 24 a row's output is 32 B per pass-B slab, and HBM
+// absorbs such scattered 32-B runs at 1.9-2.2 TB/s when the four rows of each 128-B line come from
+// different CTAs at different times (k_passAr-style items, four X-strings of one row), but at
+// 3.3-3.7 TB/s when the four units of one CTA write them together (tools/microbench_wr.cu,
+// profiles/r02_microbench_write_patterns.txt).  CTA-staged whole-line stores (4.5 TB/s alone) and
+// 2-CTA clusters sharing psi rows over DSMEM measured slower here: their CTA/cluster barriers cost
+// more than the write pattern saves.
 // Items run X-string-fastest, so the K X-strings of a launch read each psi row pair from L2 after
 // its first HBM fetch.
 // ------------------------------------------------------------------------------------------
@@ -972,7 +1034,6 @@ constexpr int PAQ_NS = 3;                                             // ring st
 constexpr int PAQ_CH = 256;                                           // complex per chunk
 constexpr int PAQ_SMEM = 4 * PAQ_NS * 2 * PAQ_CH * 16 + 4 * 4096 * 8;  // 96 KB rings + 128 KB transposes
 __device__ __forceinline__ uint32_t xsw12(uint32_t e) { return e ^ ((e >> 6) & 15u); }
-__device__ __forceinline__ uint32_t xsw16(uint32_t c) { return c ^ ((c >> 7) & 7u); }   // 16-B chunks of the staging
 __device__ __forceinline__ void tmem_st4d(uint32_t ta, const double (&v)[4]) {         // 4 doubles -> 8 columns
   asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%8], {%0, %1, %2, %3, %4, %5, %6, %7};\n"
                ::"r"(__double2loint(v[0])), "r"(__double2hiint(v[0])), "r"(__double2loint(v[1])), "r"(__double2hiint(v[1])),
@@ -982,15 +1043,14 @@ __device__ __forceinline__ void tmem_st4d(uint32_t ta, const double (&v)[4]) {  
 
 template <int N>
 __global__ void __launch_bounds__(256, 1) k_passAq(const double2* __restrict__ psi, uint64_t a_first, int kcount,
-                                                   double* __restrict__ ws) {
+                                                   uint64_t kmagic, double* __restrict__ ws) {
   constexpr int L = 12, H = N - 1 - L, CB = 13 - H;
   static_assert(H >= 8 && H <= 11, "k_passAq covers N = 21..24");
   constexpr uint64_t RBLK = 1ull << (H - 2);                          // 4-row blocks per plane
   constexpr size_t PLANE = (size_t)1 << (N - 1);
-  constexpr int QB = CB - 2;                                          // 32-B pieces per slab row = 2^QB
   extern __shared__ __align__(128) double smem[];
   double2* rings = reinterpret_cast<double2*>(smem);                 // [unit][NS][q 256 | r 256]
-  double* exch = smem + 4 * PAQ_NS * 2 * PAQ_CH * 2;                  // [unit][4096]; all four = staging
+  double* exch = smem + 4 * PAQ_NS * 2 * PAQ_CH * 2;                  // [unit][4096]
   __shared__ __align__(8) uint64_t full[4][PAQ_NS];
   __shared__ int used[4][PAQ_NS];
   __shared__ uint32_t tmem_s;
@@ -1000,6 +1060,12 @@ __global__ void __launch_bounds__(256, 1) k_passAq(const double2* __restrict__ p
   const uint64_t items = RBLK * (uint64_t)kcount;
   const uint64_t my_items = items > blockIdx.x ? (items - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const uint64_t stages = my_items * 16;
+  // item -> (m, k) = (item / kcount, item % kcount) without a division: kmagic = ceil(2^40 / kcount),
+  // exact for item < 2^40 / kcount^2 (items <= 2^9 x 512 here)
+  auto split = [&](uint64_t item, uint64_t& m, uint64_t& k) {
+    m = (item * kmagic) >> 40;
+    k = item - m * (uint64_t)kcount;
+  };
   if (w == 0) tmem_alloc(&tmem_s, 256);
   if (threadIdx.x == 32) {
     for (int x = 0; x < 4; ++x)
@@ -1012,10 +1078,10 @@ __global__ void __launch_bounds__(256, 1) k_passAq(const double2* __restrict__ p
   const uint32_t tm = tmem_s + ((uint32_t)(32 * (w & 3)) << 16) + 128u * (uint32_t)(w >> 2);
   double2* ring = rings + (size_t)u * PAQ_NS * 2 * PAQ_CH;
   auto produce = [&](uint64_t s, int slot) {                        // one thread of unit u
-    const uint64_t item = blockIdx.x + (s >> 4) * gridDim.x;
+    uint64_t m, kk;
+    split(blockIdx.x + (s >> 4) * gridDim.x, m, kk);
     const uint32_t c = (uint32_t)(s & 15);
-    const uint64_t m = item / (uint64_t)kcount;
-    const uint64_t a = a_first + item % (uint64_t)kcount;
+    const uint64_t a = a_first + kk;
     const int p = 63 - __clzll((long long)a);                        // >= 12
     const uint64_t xh = ins0(4 * m + u, p - L);
     const uint32_t ahi = (uint32_t)((a >> 8) & 15u);
@@ -1031,9 +1097,8 @@ __global__ void __launch_bounds__(256, 1) k_passAq(const double2* __restrict__ p
   const BarNamed bar{1 + u, 64};
   uint64_t s = 0;
   for (uint64_t li = 0; li < my_items; ++li) {
-    const uint64_t item = blockIdx.x + li * gridDim.x;
-    const uint64_t m = item / (uint64_t)kcount;
-    const uint64_t k = item % (uint64_t)kcount;
+    uint64_t m, k;
+    split(blockIdx.x + li * gridDim.x, m, k);
     const uint32_t al = (uint32_t)((a_first + k) & 4095u);
     const uint32_t alo = al & 63u, ajq = (al >> 6) & 3u;
     double v[64];
@@ -1061,7 +1126,7 @@ __global__ void __launch_bounds__(256, 1) k_passAq(const double2* __restrict__ p
       }
     }
     tmem_wait_st();
-    double* wk = ws + (size_t)k * 2 * PLANE + (m << (CB + 2));         // rows 4m.. of slab 0
+    double* wr = ws + (size_t)k * 2 * PLANE + ((4 * m + u) << CB);    // row 4m + u of slab 0
     auto transform_store = [&](double* wp) {
       bfly64(v);                                         // round 0: pos bits 6..11
       bar.sync();                                        // previous readers of xb are done
@@ -1071,29 +1136,14 @@ __global__ void __launch_bounds__(256, 1) k_passAq(const double2* __restrict__ p
 #pragma unroll
       for (int j = 0; j < 64; ++j) v[j] = xb[xsw12(64u * t + j)];
       bfly64(v);                                         // round 1: pos bits 0..5
-      // staging (16-B chunks, workspace order): piece g = (slab, row u, sub-piece q) of 4 doubles
-      __syncthreads();                                   // every unit is done with its transpose buffer
-      double2* st2 = reinterpret_cast<double2*>(exch);
 #pragma unroll
-      for (int r = 0; r < 16; ++r) {
-        const uint32_t pc = 16u * t + r;                 // piece of this row: pos = 4 pc .. 4 pc + 3
-        const uint32_t g = (((pc >> QB) * 4u + (uint32_t)u) << QB) + (pc & ((1u << QB) - 1u));
-        st2[xsw16(2 * g)] = make_double2(v[4 * r], v[4 * r + 1]);
-        st2[xsw16(2 * g + 1)] = make_double2(v[4 * r + 2], v[4 * r + 3]);
+      for (int r4 = 0; r4 < 16; ++r4) {
+        const uint32_t pos = 64u * t + 4u * r4;
+        const size_t off = ((size_t)(pos >> CB) << (H + CB)) + (pos & ((1u << CB) - 1u));
+        stg_v4(wp + off, v[4 * r4], v[4 * r4 + 1], v[4 * r4 + 2], v[4 * r4 + 3]);
       }
-      __syncthreads();
-      // chunk C -> piece g = C >> 1 -> (slab g >> (QB + 2), rows 4m.., offset within the slab's 4-row run)
-#pragma unroll 8
-      for (int i = 0; i < 32; ++i) {
-        const uint32_t C = threadIdx.x + 256u * i;
-        const uint32_t g = C >> 1;
-        const size_t off = ((size_t)(g >> (QB + 2)) << (H + CB)) + 4u * (g & ((4u << QB) - 1u)) + 2u * (C & 1u);
-        const double2 x = st2[xsw16(C)];
-        __stcg(reinterpret_cast<double2*>(wp + off), x);
-      }
-      __syncthreads();                                   // staging read by every unit before the next transpose
     };
-    transform_store(wk);                                 // plane A
+    transform_store(wr);                                 // plane A
 #pragma unroll
     for (int c = 0; c < 8; ++c) {                        // plane B back from TMEM
       uint32_t r32[16];
@@ -1102,7 +1152,7 @@ __global__ void __launch_bounds__(256, 1) k_passAq(const double2* __restrict__ p
 #pragma unroll
       for (int i = 0; i < 8; ++i) v[8 * c + i] = __hiloint2double(r32[2 * i + 1], r32[2 * i]);
     }
-    transform_store(wk + PLANE);                         // plane B
+    transform_store(wr + PLANE);                         // plane B
   }
   tmem_fence_before();
   __syncthreads();
@@ -1110,9 +1160,9 @@ __global__ void __launch_bounds__(256, 1) k_passAq(const double2* __restrict__ p
 }
 
 // ------------------------------------------------------------------------------------------
-// Radix-64 pass B over 2^13-double tiles (N = 21..24, FP64): k_passBr<CB>.  A tile is the
+// Radix-64 pass B over 2^13-double tiles (FP64, N = 17..24): k_passBr<CB, L>.  A tile is the
 // contiguous slab of 2^H rows x 2^CB columns (H + CB = 13, element e = row * 2^CB + col) that
-// k_passAq wrote; a unit of 128 threads holds it as 64 values per thread, so the H row bits take
+// k_passA10s (L = 10) or k_passAq (L = 12) wrote; a unit of 128 threads holds it as 64 values per thread, so the H row bits take
 // two register rounds and ONE transpose (k_passBt<13, CB>: 32 values, three rounds).
 //   Round 0: registers = e bits 7..12 (the 6 high row bits), thread = e bits 0..6 (pos = t + 128 j).
 //   Round 1: registers = e bits 1..6 (the remaining H - 6 row bits and CB - 1 column bits),
@@ -1125,11 +1175,11 @@ __global__ void __launch_bounds__(256, 1) k_passAq(const double2* __restrict__ p
 constexpr int PBR_SMEM = 3 * 8192 * 8;
 __device__ __forceinline__ uint32_t xsw13(uint32_t e) { return e ^ (((e >> 7) & 7u) << 1); }
 
-template <int CB, bool A2>
+template <int CB, int L, bool A2>
 __global__ void __launch_bounds__(256, 1) k_passBr(int kcount, const double* __restrict__ ws, Alphas al,
                                                    double* partial) {
-  constexpr int H = 13 - CB, L = 12;
-  static_assert(H >= 8 && H <= 11, "k_passBr covers N = 21..24");
+  constexpr int H = 13 - CB;
+  static_assert(H >= 6 && H <= 11, "k_passBr: 6 to 11 row bits (N = 17..20 with L = 10, N = 21..24 with L = 12)");
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t full[3];
   __shared__ volatile unsigned long long issued[3];
@@ -1197,6 +1247,20 @@ __global__ void __launch_bounds__(256, 1) k_passBr(int kcount, const double* __r
       }
     tile_accumulate<A2>(acc, v, al);
     if (al.hist) spec_add(shist, v);
+    if (al.chi) {     // sre_chi: register j holds tile element e = (t & 1) | (j << 1) | ((t >> 1) << 7)
+      const uint64_t tile = blockIdx.x + n * gridDim.x;
+      const uint64_t kp = tile / slabs, slab = tile % slabs;
+      const uint64_t a = al.chi_a0 + (kp >> 1);
+      const int p = pivot_of(a, L + H + 1);
+#pragma unroll
+      for (int j = 0; j < 64; ++j) {
+        const uint32_t e = tb | ((uint32_t)j << 1);
+        const uint64_t pos = (slab << CB) | (e & ((1u << CB) - 1u));
+        // k_passAq: position = frequency; k_passA10s: frequency 32 lane + j sits at pos = lane + 32 j
+        const uint64_t bl = L == 10 ? (((pos & 31) << 5) | (pos >> 5)) : pos;
+        chi_store(al.chi, a, p, (int)(kp & 1), ((uint64_t)(e >> CB) << L) | bl, v[j]);
+      }
+    }
   }
   block_flush(acc, partial, blockIdx.x);
   if (al.hist) {

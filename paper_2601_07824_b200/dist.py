@@ -32,9 +32,32 @@ def exact_sharded(n: int, alphas: Sequence[float], rank: int, world: int,
     return finalize_fn(sums)
 
 
+def state_shard(b: int, rank: int, world: int):
+    """Contiguous shard [s0, s1) of a batch of b states for rank `rank` (may be empty when b < world)."""
+    return shard_bounds(b, rank, world)
+
+
+def exact_batched_sharded(n: int, b: int, alphas: Sequence[float], rank: int, world: int,
+                          partial_fn: Callable, allreduce_fn: Callable, finalize_fn: Callable, zeros_fn: Callable):
+    """Batched states sharded over ranks (256 states / 8 GPUs = 32 per GPU): rank g
+    evaluates every X-string of states [g b / G, (g+1) b / G) -- whole, independent problems
+     -- into its rows of a zeroed [b, n_alpha+2] buffer; ONE all_reduce(SUM) assembles
+    the batch (each row has exactly one nonzero contributor, so the sum is exact and deterministic).
+    partial_fn(s0, s1) -> sums [s1 - s0, n_alpha+2]; zeros_fn(b, k) -> zeroed buffer."""
+    s0, s1 = state_shard(b, rank, world)
+    buf = zeros_fn(b, len(alphas) + 2)
+    if s1 > s0:
+        buf[s0:s1] = partial_fn(s0, s1)
+    allreduce_fn(buf)
+    return finalize_fn(buf)
+
+
 def exact(psi, alphas: Sequence[float] = (2.0,), group=None, workspace=None):
     """M_alpha and lost_norm of psi (cuda complex128 tensor [2^N] or [B, 2^N], identical on every
-    rank) using every rank of `group`.  Returns numpy (M [B][n_alpha], lost_norm [B]) on all ranks."""
+    rank) using every rank of `group`.  Returns numpy (M [B][n_alpha], lost_norm [B]) on all ranks.
+    A batch with at least as many states as ranks is sharded by state; otherwise every state's
+    X-strings are sharded."""
+    import torch
     import torch.distributed as dist
 
     from . import finalize, partial_sums
@@ -42,13 +65,22 @@ def exact(psi, alphas: Sequence[float] = (2.0,), group=None, workspace=None):
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     n = psi.shape[-1].bit_length() - 1
-
-    def part(lo, hi):
-        return partial_sums(psi, lo, hi, alphas, workspace=workspace)
+    b = 1 if psi.dim() == 1 else psi.shape[0]
 
     def allreduce(t):
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+
+    if b >= world and world > 1:
+        def part_states(s0, s1):
+            return partial_sums(psi[s0:s1], 0, 1 << n, alphas, workspace=workspace)
+
+        return exact_batched_sharded(n, b, alphas, rank, world, part_states, allreduce,
+                                     lambda s: finalize(s, n, alphas),
+                                     lambda bb, k: torch.zeros((bb, k), dtype=torch.float64, device=psi.device))
+
+    def part(lo, hi):
+        return partial_sums(psi, lo, hi, alphas, workspace=workspace)
 
     return exact_sharded(n, alphas, rank, world, part, allreduce, lambda s: finalize(s, n, alphas))
 

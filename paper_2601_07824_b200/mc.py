@@ -41,17 +41,21 @@ def energies(psi, a_list, epsilon: float = 0.0, workspace=None):
     return -np.log(s)
 
 
-def mc_sre(psi, L: int = 21, n_samples: int = 1000, burn_in: int | None = None, seed: int = 0,
-           move_width: int = 1, epsilon: float = 0.0, streams=None):
+def mc_sre(psi, L: int = 21, n_samples: int = 1000, burn_in: int | None = None, streams=None,
+           epsilon: float = 0.0):
     """Alg. 3: returns dict(m2, stderr, mean_f[L], var_f[L], acc_rate[L], betas, weights).
-    stderr follows Eq. (27)/(28) with per-chain variances of the mean from batch means."""
-    import sre_inputs as si
+    stderr follows Eq. (27)/(28) with per-chain variances of the mean from batch means.
+    streams = (init[L], flips[steps, L, width], uniforms[steps, L]): the random numbers of the chains,
+    drawn by the caller (the product draws none itself)."""
     import torch
 
     n = psi.shape[-1].bit_length() - 1
     burn = 10 * n if burn_in is None else burn_in
     steps = burn + n_samples
-    init, flips, uni = streams if streams is not None else si.mc_streams(seed, L, steps, n, move_width)
+    if streams is None:
+        raise ValueError("streams=(init, flips, uniforms) is required: the sampler consumes random numbers drawn "
+                         "by the caller (e.g. sre_inputs.mc_streams(seed, L, burn_in + n_samples, N, move_width))")
+    init, flips, uni = streams
     betas = np.linspace(0.0, 1.0, L)
     w = simpson_weights(L)
     ws = None
@@ -78,7 +82,14 @@ def mc_sre(psi, L: int = 21, n_samples: int = 1000, burn_in: int | None = None, 
     bsz = n_samples // nb
     bm = hist[: nb * bsz].reshape(nb, bsz, L).mean(axis=1)
     var_mean = bm.var(axis=0, ddof=1) / nb
-    m2 = float(np.dot(w, mean_f) / math.log(2.0))
-    stderr = float(math.sqrt(np.dot(w * w, var_mean)) / math.log(2.0))
+    # Eq. (M2_TI_reg_explicit_correct), in reading C16's sign: I = sum_l w_l <f>_l = ln Z_0 - ln Z_1
+    # with Z_1 = S_2 + 2^N eps, so M_2 = -log2(e^{-I} - eps) (= I / ln 2 at eps = 0); the error propagates
+    # with dM_2/dI = e^{-I} / ((e^{-I} - eps) ln 2) (Eq. (m2error), at eps = 0)
+    integral = float(np.dot(w, mean_f))
+    z = math.exp(-integral) - epsilon
+    if z <= 0.0:
+        raise ValueError("e^{-I} <= eps: the estimate is outside the regularised range (P:469-474)")
+    m2 = -math.log2(z)
+    stderr = float(math.sqrt(np.dot(w * w, var_mean)) * math.exp(-integral) / (z * math.log(2.0)))
     return {"m2": m2, "stderr": stderr, "mean_f": mean_f, "var_f": hist.var(axis=0), "acc_rate": acc / n_samples,
             "betas": betas, "weights": w, "final_patterns": a}

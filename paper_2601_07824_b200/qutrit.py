@@ -14,7 +14,7 @@ import ctypes
 
 import numpy as np
 
-from . import SreError, _check, load
+from . import SreError, _bind_stream, _check, load
 
 _ready = False
 
@@ -96,6 +96,7 @@ def partial_sums(psi, a_begin: int, a_end: int, out=None, workspace=None, stream
     if workspace is None or workspace.numel() < need:
         workspace = torch.empty(need, dtype=torch.uint8, device=dev)
     st = stream if stream is not None else torch.cuda.current_stream(dev)
+    _bind_stream(st, psi, keep, out, workspace)
     _check(lib.sre_mana_partial_sums(ctypes.c_void_p(ptr), n, int(a_begin), int(a_end),
                                      ctypes.c_void_p(workspace.data_ptr()), workspace.numel(),
                                      ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(st.cuda_stream)))
@@ -158,6 +159,7 @@ def mixed_sums_(rho_flat, n: int, out=None, workspace=None, stream=None):
     if workspace is None or workspace.numel() < need:
         workspace = torch.empty(need, dtype=torch.uint8, device=dev)
     st = stream if stream is not None else torch.cuda.current_stream(dev)
+    _bind_stream(st, rho_flat, rho_flat, out, workspace)
     _check(lib.sre_mana_mixed_sums(ctypes.c_void_p(rho_flat.data_ptr()), n, ctypes.c_void_p(workspace.data_ptr()),
                                    workspace.numel(), ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(st.cuda_stream)))
     return out

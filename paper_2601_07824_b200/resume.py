@@ -29,12 +29,23 @@ def _save(path, journal):
     os.replace(tmp, path)
 
 
+def state_fingerprint(psi) -> str:
+    """sha256 of the state's amplitudes (host bytes of the complex128 vector): the journal key that
+    stops a restart with another state from reusing stored chunk sums."""
+    import hashlib
+    a = psi.detach().cpu().numpy() if hasattr(psi, "detach") else np.asarray(psi)
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
 def chunked_sums(n: int, alphas: Sequence[float], partial_fn: Callable, lo: int = 0, hi: int | None = None,
-                 chunk: int = 1 << 16, journal_path: str | None = None, max_chunks: int | None = None):
+                 chunk: int = 1 << 16, journal_path: str | None = None, max_chunks: int | None = None,
+                 state_id: str = "", precision: str = "fp64"):
     """Sum partial_fn(a0, a1) -> array[n_alpha+2] over [lo, hi) in chunks, journaled.
-    Returns (sums, complete) where complete is False if max_chunks stopped the sweep early."""
+    Returns (sums, complete) where complete is False if max_chunks stopped the sweep early.
+    The journal is keyed by (n, alphas, range, chunk, state_id, precision); a mismatch raises."""
     hi = (1 << n) if hi is None else hi
-    key = {"n": n, "alphas": list(map(float, alphas)), "lo": lo, "hi": hi, "chunk": chunk}
+    key = {"n": n, "alphas": list(map(float, alphas)), "lo": lo, "hi": hi, "chunk": chunk, "state": state_id,
+           "precision": precision}
     journal = _load(journal_path)
     if journal and journal.get("key") != key:
         raise ValueError(f"journal {journal_path} belongs to a different run: {journal.get('key')}")
@@ -60,20 +71,22 @@ def chunked_sums(n: int, alphas: Sequence[float], partial_fn: Callable, lo: int 
 
 
 def exact_resumable(psi, alphas: Sequence[float] = (2.0,), chunk: int = 1 << 16, journal_path: str | None = None,
-                    max_chunks: int | None = None):
+                    max_chunks: int | None = None, precision: str = "fp64"):
     """M_alpha and lost_norm of a cuda state through journaled chunks of sre_partial_sums.
     Returns (M list, lost_norm) when complete, else None (call again to continue)."""
     import torch
 
     from . import finalize, partial_sums, workspace_size
     n = psi.shape[-1].bit_length() - 1
-    ws = torch.empty(workspace_size(n, 1, len(alphas)), dtype=torch.uint8, device=psi.device)
+    ws = torch.empty(workspace_size(n, 1, len(alphas), precision), dtype=torch.uint8, device=psi.device)
 
     def part(a0, a1):
-        out = partial_sums(psi, a0, a1, alphas, workspace=ws)
+        out = partial_sums(psi, a0, a1, alphas, workspace=ws, precision=precision)
         return out.cpu().numpy()[0]
 
-    sums, complete = chunked_sums(n, alphas, part, chunk=chunk, journal_path=journal_path, max_chunks=max_chunks)
+    sid = state_fingerprint(psi) if journal_path else ""
+    sums, complete = chunked_sums(n, alphas, part, chunk=chunk, journal_path=journal_path, max_chunks=max_chunks,
+                                  state_id=sid, precision=precision)
     if not complete:
         return None
     m, ln = finalize(sums, n, alphas)

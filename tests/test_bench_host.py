@@ -42,3 +42,28 @@ def test_bench_traffic_lookup():
             assert bench.ncu_traffic(cfg, t["kind"]) == t["dram_bytes_per_launch"] > 0
             other = "pass_b" if t["kind"] != "pass_b" else "pass_a"
             assert bench.ncu_traffic(cfg, other) is None
+
+
+def test_roofline_accounting():
+    """Algorithmic bytes/ops of the bench line: pass A = 8 B/Pauli + one psi read
+    per launch, pass B = 8 B/Pauli, L = 10 (N <= 20) / 12 (N = 21..24) / 13 (N = 25); at N = 24 a pass A
+    moving its bytes at exactly the HBM peak reads frac 1 (it cannot exceed 1 at any slower time)."""
+    bench = _load("bench_mod", "bench.py")
+    peaks = {"hbm_gbs": 6551.4}
+    assert [bench.two_pass_L(n) for n in (15, 20, 21, 24, 25)] == [10, 10, 12, 12, 13]
+    k = 32
+    paulis = k * float(1 << 24)
+    bytes_a = 8.0 * paulis + 16.0 * (1 << 24)
+    t_ms = bytes_a / 6551.4e9 * 1e3
+    r = bench.roofline(24, 1, [2.0], "pass_a", t_ms, paulis, peaks, "measured", 1965.0)
+    assert r["bound"] == "hbm" and abs(r["frac"] - 1.0) < 1e-12
+    assert abs(r["bytes_per_pauli"] - (8.0 + 16.0 / k)) < 1e-12
+    assert r["fp64"]["ops_per_pauli"] == 2 + 12
+    rb = bench.roofline(20, 1, [2.0], "pass_b", 1.0, 128 * float(1 << 20), peaks, "measured", 1965.0)
+    assert rb["bytes_per_pauli"] == 8.0 and rb["fp64"]["ops_per_pauli"] == (20 - 1 - 10) + 3
+    rs = bench.roofline(14, 256, [2.0], "single_pass", 1.0, 1e9, peaks, "measured", 1965.0)
+    assert rs["bound"] == "alu" and rs["ops_per_pauli"] == 2 + 13 + 3
+    # alpha in {1, 2, 3}: log (26) + t ln t FMA (1) + alpha 2 (2) + alpha 3 (3) on top of t and purity (2)
+    assert bench.epilogue_ops([1.0, 2.0, 3.0]) == 2 + 26 + 1 + 2 + 3
+    assert bench.epilogue_ops([2.0]) == 3
+    assert bench.epilogue_ops([0.5]) == 2 + 26 + 22

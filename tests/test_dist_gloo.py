@@ -127,3 +127,60 @@ def test_gloo_mana_sharded_equals_single(world):
     bounds = [sdist.shard_bounds(3 ** n, r, world) for r in range(world)]
     assert bounds[0][0] == 0 and bounds[-1][1] == 3 ** n
     assert all(bounds[i][1] == bounds[i + 1][0] for i in range(world - 1))
+
+
+def _batch_worker(rank, world, port, n, b, alphas, out_q):
+    import torch.distributed as dist
+
+    import oracle
+    import paper_2601_07824_b200 as sre
+    from paper_2601_07824_b200 import dist as sdist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    batch = si.haar_batch(n, b, 779)
+    seen = []
+
+    def part(s0, s1):
+        seen.append((s0, s1))
+        return torch.from_numpy(np.stack([oracle.sums_fwht(batch[s], alphas) for s in range(s0, s1)]))
+
+    def allreduce(t):
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+
+    m, ln = sdist.exact_batched_sharded(n, b, alphas, rank, world, part, allreduce,
+                                        lambda s: sre.finalize(s.numpy(), n, alphas),
+                                        lambda bb, k: torch.zeros((bb, k), dtype=torch.float64))
+    out_q.put((rank, m.tolist(), ln.tolist(), seen))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_state_sharded_batch(world):
+    """Batched variant sharded by state: 5 states over 2 or 3 ranks (ragged shards), one
+    all_reduce of the zero-padded [B, n_alpha+2] sums; every rank returns the whole batch's M."""
+    import torch.multiprocessing as mp
+
+    import oracle
+    oracle.build()
+    n, b, alphas = 6, 5, [1.0, 2.0]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_batch_worker, args=(r, world, port, n, b, alphas, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    batch = si.haar_batch(n, b, 779)
+    ref = [oracle.sre(batch[s], alphas, "fwht") for s in range(b)]
+    shards = sorted(sh for _, _, _, seen in res for sh in seen)
+    assert shards[0][0] == 0 and shards[-1][1] == b and all(shards[i][1] == shards[i + 1][0] for i in range(len(shards) - 1))
+    for _, m, ln, _ in res:
+        for s in range(b):
+            assert np.max(np.abs(np.array(m[s]) - np.array(ref[s][0]))) < 1e-12
+            assert abs(ln[s] - ref[s][1]) < 1e-13

@@ -56,7 +56,7 @@ def test_sampler_estimates_exact_m2(sre, oracle_lib):
     t = torch.from_numpy(psi).cuda()
     exact = sre.exact(t, [2.0])[0][0]
     quad = omc.ti_exact(psi, L)                   # same quadrature, zero MC error
-    r = mc.mc_sre(t, L=L, n_samples=2000, seed=5)
+    r = mc.mc_sre(t, L=L, n_samples=2000, streams=si.mc_streams(5, L, 10 * n + 2000, n, 1))
     assert abs(quad - exact) < 0.05
     assert abs(r["m2"] - quad) < 6 * r["stderr"] + 1e-3
     assert r["acc_rate"][0] == 1.0

@@ -76,9 +76,8 @@ def test_two_pass_ranges_vs_oracle(sre, oracle_lib, n):
 @pytest.mark.parametrize("n", [21, 22, 23, 24])
 def test_streamed_production_batches_vs_oracle(sre, oracle_lib, n):
     """N = 21..24 at the production launch size: a full K-aligned batch (K = 64 at N = 21, 32 above)
-    runs the radix-64 pass A (k_passAr, every group of 4 active) and the TMA pass B; a second range
-    ends mid-group (kcount = 8 m + 5: the last group of 4 has one active X-string) and a third covers
-    an a_h with a high pivot.  Raw sums vs the Alg. 2 oracle at 1e-10 for alpha = 1, 2, 3."""
+    runs the radix-64 pass A (k_passAq) and pass B (k_passBr); a second range has an odd batch
+    (kcount = 13) and a third covers an a_h with a high pivot.  Raw sums vs the Alg. 2 oracle at 1e-10 for alpha = 1, 2, 3."""
     psi = si.haar(n, 4100 + n)
     K = 64 if n == 21 else 32
     D = 1 << n
@@ -91,13 +90,20 @@ def test_streamed_production_batches_vs_oracle(sre, oracle_lib, n):
         assert abs(g[-1] - o[-1]) <= 1e-10 * abs(o[-1]), (lo, hi)
 
 
-@pytest.mark.parametrize("n", [1, 2, 5, 6, 10, 11, 13, 14, 15, 17, 20])
+@pytest.mark.parametrize("n", [1, 2, 5, 6, 10, 11, 13, 14, 15, 17, 20, 21, 23, 24])
 def test_chi_elementwise(sre, oracle_lib, n):
-    """chi_b(a) for every b, sampled a, element by element against the oracle's Alg. 2 transform."""
+    """chi_b(a) for every b, sampled a, element by element against the oracle's Alg. 2 transform.
+    For N >= 15 the 8-aligned a >= 2^L run the production kernels of the sums (staged k_passA10s +
+    k_passBt, streamed k_passAq + k_passBr), the others the generic head kernels."""
     psi = si.haar(n, 3000 + n)
     D = 1 << n
     rng = np.random.default_rng(n)
     a_list = sorted({0, 1, D - 1, *[int(x) for x in rng.integers(0, D, 3)]})
+    if n >= 15:
+        lo = 1 << (10 if n <= 20 else 12)
+        a_list = sorted(set(a_list) | {lo, D - 8, *[8 * int(x) for x in rng.integers(lo // 8, D // 8, 3)]})
+    if n >= 23:
+        a_list = [a for a in a_list if a % 8 == 0 and a >= 4096][:3] + [1]
     t = cuda(psi)
     for a in a_list:
         g = sre.chi(t, a).cpu().numpy()
@@ -158,21 +164,22 @@ def test_sharded_ranges_sum_to_full(sre):
             assert rel(parts[:-1], full[:-1]) < 1e-13
 
 
-def test_batched_config3_sampled(sre, oracle_lib):
-    """BASELINE config 3 shape (N=14 Clifford+T batch) on 16 states: T-doped closed forms on every
-    state of that kind, oracle ranges for the interleaved ones."""
-    batch, ts = si.config3_batch(14, 16, 14000)
-    idx = list(range(4)) + list(range(8, 12))
-    sub = batch[[i for i in range(16)]]
-    m, ln = sre.exact_batched(cuda(sub), [2.0])
-    for i in range(16):
-        assert abs(ln[i]) < 1e-10
-        if ts[i] is not None:
-            assert abs(m[i, 0] - oracle_lib.t_state_m(2.0, ts[i])) < 1e-10
-    g = sre.partial_sums(cuda(sub), 100, 164, [2.0]).cpu().numpy()
-    for i in idx:
-        o = oracle_lib.sums_fwht(sub[i], [2.0], a_range=(100, 164))
-        assert rel(g[i, :1], o[:1]) < 1e-10
+def test_batched_config3_full(sre, oracle_lib):
+    """BASELINE config 3 in full (256 x N=14 Clifford+T, the bench batch): every T-doped state against
+    its closed form M_2 = t M_2(|T>), every interleaved state's sums over an X-string
+    range against the oracle, and every lost_norm."""
+    batch, ts = si.config3_batch(14, 256, 14000)
+    m, ln = sre.exact_batched(cuda(batch), [2.0])
+    assert np.max(np.abs(ln)) < 1e-10
+    tdoped = [i for i in range(256) if ts[i] is not None]
+    assert len(tdoped) == 128
+    for i in tdoped:
+        assert abs(m[i, 0] - oracle_lib.t_state_m(2.0, ts[i])) < 1e-10, i
+    g = sre.partial_sums(cuda(batch), 100, 132, [2.0]).cpu().numpy()
+    for i in range(256):
+        if ts[i] is None:
+            o = oracle_lib.sums_fwht(batch[i], [2.0], a_range=(100, 132))
+            assert rel(g[i, :2], o[:2]) < 1e-10, i
 
 
 def test_scrambled_pair_n20(sre, oracle_lib):

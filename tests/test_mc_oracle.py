@@ -45,6 +45,18 @@ def test_ti_converges_to_exact_sre(oracle_lib, mco):
     assert errs[2] < 1e-6 and errs[2] < errs[0]
 
 
+def test_ti_regularised_converges_to_exact_sre(oracle_lib, mco):
+    """eps > 0: M_2 = -log2(e^{-I} - eps) removes the regulariser exactly, so the quadrature
+    still converges to the unregularised M_2 (a plain I / ln 2 would be biased by ~eps 2^N / S_2)."""
+    psi = si.haar(6, 31)
+    exact = oracle_lib.sre(psi, [2.0])[0][0]
+    for eps in (1e-3, 1e-2):
+        assert abs(mco.ti_exact(psi, 41, eps) - exact) < 1e-6
+        biased = sum(w * mco.mean_f_exact(mco.all_energies(psi, eps), b)
+                     for b, w in zip(*mco.simpson(41))) / math.log(2.0)
+        assert abs(biased - exact) > 1e-3
+
+
 def test_replay_chain_samples_boltzmann(mco):
     """Detailed-balance check at desk scale: a long beta = 1 chain's pattern frequencies follow
     Pi_1(a) = S(a)/S_2 (Eq. (18)) within multinomial error."""

@@ -33,3 +33,19 @@ def test_journal_key_mismatch(tmp_path):
     chunked_sums(3, [2.0], lambda a0, a1: np.zeros(3), chunk=4, journal_path=j)
     with pytest.raises(ValueError):
         chunked_sums(3, [3.0], lambda a0, a1: np.zeros(3), chunk=4, journal_path=j)
+
+
+def test_journal_rejects_other_state_or_precision(tmp_path):
+    """the key carries a state fingerprint and the precision, so a restart with another psi
+    cannot silently mix stored chunk sums of two states."""
+    import pytest
+    from paper_2601_07824_b200.resume import chunked_sums, state_fingerprint
+    a, b = si.haar(3, 1), si.haar(3, 2)
+    assert state_fingerprint(a) != state_fingerprint(b) and state_fingerprint(a) == state_fingerprint(a.copy())
+    j = str(tmp_path / "j.json")
+    chunked_sums(3, [2.0], lambda a0, a1: np.zeros(3), chunk=4, journal_path=j, state_id=state_fingerprint(a))
+    with pytest.raises(ValueError):
+        chunked_sums(3, [2.0], lambda a0, a1: np.zeros(3), chunk=4, journal_path=j, state_id=state_fingerprint(b))
+    with pytest.raises(ValueError):
+        chunked_sums(3, [2.0], lambda a0, a1: np.zeros(3), chunk=4, journal_path=j, state_id=state_fingerprint(a),
+                     precision="fp32")
