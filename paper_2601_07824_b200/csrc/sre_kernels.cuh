@@ -185,14 +185,54 @@ __device__ __forceinline__ double ln_fast(double t) {
   const bool hi = m > 1.4142135623730951;
   m = hi ? 0.5 * m : m;
   e += hi ? 1 : 0;
-  const double s = (m - 1.0) / (m + 1.0);
-  const double s2 = s * s;
-  double p = 1.0 / 19;
-  p = fma(p, s2, 1.0 / 17); p = fma(p, s2, 1.0 / 15); p = fma(p, s2, 1.0 / 13); p = fma(p, s2, 1.0 / 11);
-  p = fma(p, s2, 1.0 / 9); p = fma(p, s2, 1.0 / 7); p = fma(p, s2, 1.0 / 5); p = fma(p, s2, 1.0 / 3);
-  const double ls = fma(2.0 * s * s2, p, 2.0 * s);                                        // 2 atanh(s)
+  // s = (m - 1) / (m + 1) with a reciprocal: MUFU approximation + two Newton steps (2^-23 -> 2^-92),
+  // shorter and branch-free compared with the IEEE division sequence
+  const double y = m + 1.0;
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(y));
+  r = fma(r, fma(-y, r, 1.0), r);
+  r = fma(r, fma(-y, r, 1.0), r);
+  const double s = (m - 1.0) * r;
+  const double z = s * s, z2 = z * z, z4 = z2 * z2;
+  // 1/3 + z/5 + ... + z^8/19 by Estrin's scheme (dependency depth 4 instead of 8)
+  const double p01 = fma(1.0 / 5, z, 1.0 / 3), p23 = fma(1.0 / 9, z, 1.0 / 7);
+  const double p45 = fma(1.0 / 13, z, 1.0 / 11), p67 = fma(1.0 / 17, z, 1.0 / 15);
+  const double p03 = fma(p23, z2, p01), p47 = fma(p67, z2, p45);
+  const double p = fma(fma(1.0 / 19, z4, p47), z4, p03);
+  const double ls = fma(2.0 * s * z, p, 2.0 * s);                                         // 2 atanh(s)
   return fma((double)e, 0.6931471805599453, fma((double)e, 2.3190468138462996e-17, ls)); // e ln2 (hi + lo)
 }
+// Table-driven ln for the t ln t pass (t = y^2 <= 1/4, so ln t <= -1.38 and nothing cancels): m in
+// [1, 2) split at its top 7 mantissa bits i; r_i = RN(1 / m_i), m_i = 1 + (i + 1/2)/128, L_i = -ln r_i;
+// ln m = L_i + ln(1 + d), d = m r_i - 1 (one FMA, |d| < 2^-8), ln(1 + d) to d^7 by Estrin (truncation
+// d^8/8 < 2e-20).  11 FP64 ops against ln_fast's ~25; 1.7e-16 relative on t <= 1/4 (host check against
+// logl).  The 2 KB table lives in each CTA's shared memory, built once per launch (ln_table_init).
+__device__ __forceinline__ double2* ln_table() {
+  __shared__ double2 tab[128];
+  return tab;
+}
+__device__ __forceinline__ void ln_table_init(bool need) {   // every thread of the CTA, before any use
+  if (need) {
+    double2* tab = ln_table();
+    for (int i = threadIdx.x; i < 128; i += blockDim.x) {
+      const double r = 1.0 / (1.0 + (i + 0.5) / 128.0);
+      tab[i] = make_double2(r, -log(r));
+    }
+    __syncthreads();
+  }
+}
+__device__ __forceinline__ double ln_tab(double t) {
+  const long long b = __double_as_longlong(t);
+  const int e = (int)((b >> 52) & 0x7ff) - 1023;
+  const double2 T = ln_table()[(b >> 45) & 127];
+  const double m = __longlong_as_double((b & 0x000fffffffffffffLL) | 0x3ff0000000000000LL);
+  const double d = fma(m, T.x, -1.0), d2 = d * d;
+  const double q = fma(fma(1.0 / 7, d, -1.0 / 6), d2, fma(1.0 / 5, d, -1.0 / 4));
+  const double poly = fma(fma(q, d2, fma(1.0 / 3, d, -0.5)), d2, d);
+  return fma((double)e, 0.6931471805599453, fma((double)e, 2.3190468138462996e-17, T.y + poly));
+}
+__device__ __forceinline__ float ln_tab(float t) { return logf(t); }
+
 // e^z for z <= 0 (t^alpha = e^(alpha ln t)): z = k ln 2 + r, |r| <= ln2/2, Taylor to r^13
 // (truncation r^14/14! < 2e-17 relative); 2^k applied in two exponent steps; z < -745 -> 0.
 __device__ __forceinline__ double exp_fast(double z) {
@@ -212,10 +252,9 @@ __device__ __forceinline__ float ln_fast(float t) { return logf(t); }
 __device__ __forceinline__ float exp_fast(float z) { return expf(z); }
 
 // Epilogue of one tile's values per thread into a fresh local sum, then one add into the long-lived
-// accumulators: keeps the running-sum chains short (DESIGN "Summation").  General alphas run in
-// compact phases (integer powers + purity; t ln t if some alpha = 1; real powers if some alpha is
-// non-integer), four values per step of a rolled loop: unrolling a full tile of log/exp bodies made
-// the kernel instruction-cache bound in round 1.  Terms with t below 1e-300 add 0 (t ln t > -1e-297).
+// accumulators: keeps the running-sum chains short (DESIGN "Summation").  The general-alpha body is
+// compact (ln_fast ~30 SASS instead of the ~120 of log(), which made a full unroll I-cache bound in
+// round 1).  Terms with t below 1e-300 add 0 (t ln t > -1e-297).
 template <bool A2, class R, int M>
 __device__ __forceinline__ void tile_accumulate(double (&acc)[NACC], const R (&v)[M], const Alphas& al) {
   R loc[NACC];          // FP32 mode: local sums in FP32, one conversion per tile
@@ -224,30 +263,71 @@ __device__ __forceinline__ void tile_accumulate(double (&acc)[NACC], const R (&v
   if constexpr (A2) {
 #pragma unroll
     for (int j = 0; j < M; ++j) Epi<true, R>::add(loc, v[j], al);
+  } else if (!al.any_real) {
+    // Integer alphas (+ t ln t when some alpha = 1): registers only, unrolled passes over the tile.  The round-1 compact loop
+    // staged t through a per-thread local array, which misses L1 beside a ~200 KB smem ring (LDL
+    // long-scoreboard stalls: config 2 pass B 3.2x slower, measured); one fused per-value body over all
+    // slots grows the kernel past the instruction cache; several partial sums per pass spill at M = 64.
+    // one pass for the purity and the powers t^1..t^4 (independent sums), exponents > 4 in their own pass
+    R s1 = R(0), s2 = R(0), s3 = R(0), s4 = R(0);
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+      const R t = v[j] * v[j], t2 = t * t;
+      s1 += t;
+      s2 += t2;
+      s3 = fma(t2, t, s3);
+      s4 = fma(t2, t2, s4);
+    }
+    loc[MAXA] += s1;
+#pragma unroll
+    for (int i = 0; i < MAXA; ++i) {
+      if (i >= al.n) break;
+      const int e = al.iexp[i];
+      R sum = e == 1 ? s1 : e == 2 ? s2 : e == 3 ? s3 : s4;
+      if (e > 4) {
+        sum = R(0);
+#pragma unroll
+        for (int j = 0; j < M; ++j) {
+          const R t = v[j] * v[j];
+          R pw = t;
+          for (int k = 1; k < e; ++k) pw *= t;
+          sum += pw;
+        }
+      }
+      loc[i] += sum;
+    }
+    if (al.need_log) {                          // two interleaved sums (more spill at M = 64)
+      R l0 = R(0), l1 = R(0);
+#pragma unroll
+      for (int j = 0; j < M; ++j) {
+        const R t = v[j] * v[j];
+        const R x = t > R(1e-300) ? t * ln_tab(t) : R(0);
+        if (j & 1) l1 += x; else l0 += x;
+      }
+      loc[MAXA + 1] += l0 + l1;
+    }
   } else {
+    // some non-integer alpha (rare): a compact rolled loop over a per-thread local copy of t (unrolled
+    // exp(alpha ln t) bodies spill at M = 64)
     R tv[M];
 #pragma unroll
     for (int j = 0; j < M; ++j) tv[j] = v[j] * v[j];
 #pragma unroll 1
-    for (int j0 = 0; j0 < M; j0 += 4) {
+    for (int j = 0; j < M; ++j) {
+      const R t = tv[j];
+      loc[MAXA] += t;
+      const bool pos = t > R(1e-300);
+      const R lt = ln_fast(pos ? t : R(1));
+      if (al.need_log) loc[MAXA + 1] = fma(t, pos ? lt : R(0), loc[MAXA + 1]);
 #pragma unroll
-      for (int jj = 0; jj < 4; ++jj) {
-        const R t = tv[j0 + jj];
-        loc[MAXA] += t;
-        const bool pos = t > R(1e-300);
-        R lt = R(0);
-        if (al.need_log | al.any_real) lt = ln_fast(pos ? t : R(1));
-        if (al.need_log) loc[MAXA + 1] = fma(t, pos ? lt : R(0), loc[MAXA + 1]);
-#pragma unroll
-        for (int i = 0; i < MAXA; ++i) {
-          if (i >= al.n) break;
-          if (al.kind[i] == 0) {
-            R pw = t;
-            for (int k = 1; k < al.iexp[i]; ++k) pw *= t;
-            loc[i] += pw;
-          } else {
-            loc[i] += pos ? exp_fast(R(al.alpha[i]) * lt) : R(0);
-          }
+      for (int i = 0; i < MAXA; ++i) {
+        if (i >= al.n) break;
+        if (al.kind[i] == 0) {
+          R pw = t;
+          for (int k = 1; k < al.iexp[i]; ++k) pw *= t;
+          loc[i] += pw;
+        } else {
+          loc[i] += pos ? exp_fast(R(al.alpha[i]) * lt) : R(0);
         }
       }
     }
@@ -351,6 +431,7 @@ template <int T, bool A2, bool DEBUG, class V = double>
 __global__ void __launch_bounds__(256) k_small(const typename Cx<V>::T* __restrict__ psi_all, int N, uint64_t a0,
                                                uint64_t count, Alphas al, double* partial, double* chi,
                                                const uint64_t* __restrict__ alist, unsigned long long* hist) {
+  ln_table_init(!A2 && al.need_log && std::is_same<V, double>::value);   // t ln t pass (tile_accumulate)
   __shared__ unsigned long long shist[SPEC_BINS];   // hist != nullptr: spectrum epilogue
   if (hist) {
     for (int i = threadIdx.x; i < SPEC_BINS; i += blockDim.x) shist[i] = 0ull;
@@ -463,6 +544,7 @@ template <int T, bool A2, bool DEBUG, class V = double>
 __global__ void __launch_bounds__(256, 1) k_mid(const typename Cx<V>::T* __restrict__ psi_all, int N, uint64_t a0,
                                                 uint64_t count, Alphas al, double* partial, double* chi,
                                                 const uint64_t* __restrict__ alist, unsigned long long* hist) {
+  ln_table_init(!A2 && al.need_log && std::is_same<V, double>::value);   // t ln t pass (tile_accumulate)
   __shared__ unsigned long long shist[SPEC_BINS];   // hist != nullptr: spectrum epilogue
   if (hist) {
     for (int i = threadIdx.x; i < SPEC_BINS; i += blockDim.x) shist[i] = 0ull;
@@ -575,6 +657,7 @@ template <int TP, int CB, bool A2, bool DEBUG, class V = double>
 __global__ void __launch_bounds__(TP >= 14 ? 512 : 256, 1) k_passB(int N, int L, uint64_t a0, int kcount,
                                                                    const V* __restrict__ ws, Alphas al,
                                                                    double* partial, double* chi) {
+  ln_table_init(!A2 && al.need_log && std::is_same<V, double>::value);   // t ln t pass (tile_accumulate)
   __shared__ unsigned long long shist[SPEC_BINS];
   if (al.hist) {
     for (int i = threadIdx.x; i < SPEC_BINS; i += blockDim.x) shist[i] = 0ull;
@@ -773,6 +856,7 @@ __host__ __device__ constexpr int pbt_smem(int TP) { return PBT_NS * 256 / (1 <<
 template <int TP, int CB, bool A2, class V = double>   // TP = 12: two 128-thread units; 13: one 256-thread unit
 __global__ void __launch_bounds__(256, 1) k_passBt(int N, int kcount, const V* __restrict__ ws, Alphas al,
                                                    double* partial) {
+  ln_table_init(!A2 && al.need_log && std::is_same<V, double>::value);   // t ln t pass (tile_accumulate)
   constexpr int NT = 1 << (TP - 5), UNITS = 256 / NT, TILE = 1 << TP, SLOT = pbt_slot(TP);
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t full[UNITS][PBT_NS];
@@ -1178,6 +1262,7 @@ __device__ __forceinline__ uint32_t xsw13(uint32_t e) { return e ^ (((e >> 7) & 
 template <int CB, int L, bool A2>
 __global__ void __launch_bounds__(256, 1) k_passBr(int kcount, const double* __restrict__ ws, Alphas al,
                                                    double* partial) {
+  ln_table_init(!A2 && al.need_log && std::is_same<double, double>::value);   // t ln t pass (tile_accumulate)
   constexpr int H = 13 - CB;
   static_assert(H >= 6 && H <= 11, "k_passBr: 6 to 11 row bits (N = 17..20 with L = 10, N = 21..24 with L = 12)");
   extern __shared__ __align__(128) double smem[];
