@@ -85,11 +85,12 @@ int staged_groups(int N) {
   const char* e = getenv("SRE_KG");
   if (e && atoi(e) > 0) return atoi(e) > 1024 ? 1024 : atoi(e);
   // 8-X-string groups per staged launch pair, measured on B200: launch tails
-  // dominate small batches, so N <= 18 takes 4096 X-strings per launch (<= 8 GiB of workspace);
-  // N = 19 saturates at 512, N = 20 peaks at 128 (1 GiB).
+  // dominate small batches (N = 20 with 8 X-strings per launch pair: 6.3 us per X-string, L2-resident
+  // workspace or not), so N <= 18 takes 4096 X-strings per launch (<= 8 GiB of workspace);
+  // N = 19 saturates at 512.
   if (N <= 18) return 512;
   if (N == 19) return 64;
-  return 16;
+  return 32;   // N = 20: 256 X-strings (2 GiB) per launch pair, measured 3.47 vs 3.57 us per X-string at 128 (r02)
 }
 
 void two_pass_params(int T, int& L, int& H, int& CB) {

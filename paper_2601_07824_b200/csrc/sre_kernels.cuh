@@ -752,6 +752,105 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(b)) : "memory");
 }
 
+// ------------------------------------------------------------------------------------------
+// Tensor memory (TMEM) as a per-thread register extension.  Thread lane of warp w owns TMEM
+// lane 32 (w % 4) + lane; a double occupies two consecutive 32-bit columns.  tcgen05.ld/st
+// run on the tensor-memory datapath, not on the L1TEX data pipe the transposes saturate.
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {   // one full warp
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n"
+               ::"r"(smem_u32(dst_smem)), "r"(ncols) : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {      // same warp
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(taddr), "r"(ncols) : "memory");
+}
+__device__ __forceinline__ void tmem_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+// 8 doubles -> columns [ta, ta + 16) of this thread's lane
+__device__ __forceinline__ void tmem_st8d(uint32_t ta, const double (&v)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%16], {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15};\n"
+               ::"r"(__double2loint(v[0])), "r"(__double2hiint(v[0])), "r"(__double2loint(v[1])), "r"(__double2hiint(v[1])),
+                 "r"(__double2loint(v[2])), "r"(__double2hiint(v[2])), "r"(__double2loint(v[3])), "r"(__double2hiint(v[3])),
+                 "r"(__double2loint(v[4])), "r"(__double2hiint(v[4])), "r"(__double2loint(v[5])), "r"(__double2hiint(v[5])),
+                 "r"(__double2loint(v[6])), "r"(__double2hiint(v[6])), "r"(__double2loint(v[7])), "r"(__double2hiint(v[7])),
+                 "r"(ta) : "memory");
+}
+// columns [ta, ta + 16) -> 8 doubles (no wait: the caller issues tmem_wait_ld before use)
+__device__ __forceinline__ void tmem_ld8d(uint32_t ta, uint32_t (&u)[16]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];\n"
+               : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7]),
+                 "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]), "=r"(u[14]), "=r"(u[15])
+               : "r"(ta) : "memory");
+}
+__device__ __forceinline__ void stg_v4(double* p, double a, double b, double c, double d) {   // one 32-B sector
+  asm volatile("st.global.cg.v4.f64 [%0], {%1, %2, %3, %4};\n" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+
+// ------------------------------------------------------------------------------------------
+// Warp-local 10-bit transform of two 1024-point planes with the transposes in TMEM (k_passA10s, FP64).
+// Start: lane l, register j holds element e = l + 32 j.  Round 0 butterflies e bits 5..9.  A "trip"
+// stores the 32 doubles with tcgen05.st 32x32b (lane l, double column j) and reads them back with two
+// tcgen05.ld 16x256b.x8 (lane bases 0, 16): thread t = t0 + 4 t1 receives lane 16b + 8s + t1, double
+// column 4c + t0 into register r = s + 2c + 16b (CUTLASS Copy_Traits<SM100_TMEM_LOAD_16dp256b1x>).
+// Each trip brings two new element bits into the register index (tools/microbench_tmem_transpose.cu
+// verifies the map on B200): trip 1 -> e3 (r0), e4 (r4); trip 2 -> e1 (r0), e2 (r4); trip 3 -> e0 (r4).
+// After trip 3, (lane t, register r) holds frequency pa10_freq(t + 32 r).  The TMEM datapath runs
+// beside the L1TEX pipe the generation loads and stores saturate (microbenchmark: a transpose split
+// between the two costs 0.075 clk/value vs 0.126 for shared memory alone).
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t pa10_freq(uint32_t pos) {
+  const uint32_t t = pos & 31u, r = pos >> 5;
+  return ((t & 1u) << 1) | (((t >> 1) & 1u) << 8) | (((t >> 2) & 1u) << 3) | (((t >> 3) & 1u) << 7) |
+         (((t >> 4) & 1u) << 5) | ((r & 1u) << 6) | (((r >> 1) & 1u) << 9) | (((r >> 2) & 1u) << 4) |
+         (((r >> 3) & 1u) << 2) | ((r >> 4) & 1u);
+}
+__device__ __forceinline__ void tmem_st32d(uint32_t ta, const double (&v)[32]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x64.b32 [%64], {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32, %33, %34, %35, %36, %37, %38, %39, %40, %41, %42, %43, %44, %45, %46, %47, %48, %49, %50, %51, %52, %53, %54, %55, %56, %57, %58, %59, %60, %61, %62, %63};\n"
+               ::"r"(__double2loint(v[0])), "r"(__double2hiint(v[0])), "r"(__double2loint(v[1])), "r"(__double2hiint(v[1])), "r"(__double2loint(v[2])), "r"(__double2hiint(v[2])), "r"(__double2loint(v[3])), "r"(__double2hiint(v[3])),
+                 "r"(__double2loint(v[4])), "r"(__double2hiint(v[4])), "r"(__double2loint(v[5])), "r"(__double2hiint(v[5])), "r"(__double2loint(v[6])), "r"(__double2hiint(v[6])), "r"(__double2loint(v[7])), "r"(__double2hiint(v[7])),
+                 "r"(__double2loint(v[8])), "r"(__double2hiint(v[8])), "r"(__double2loint(v[9])), "r"(__double2hiint(v[9])), "r"(__double2loint(v[10])), "r"(__double2hiint(v[10])), "r"(__double2loint(v[11])), "r"(__double2hiint(v[11])),
+                 "r"(__double2loint(v[12])), "r"(__double2hiint(v[12])), "r"(__double2loint(v[13])), "r"(__double2hiint(v[13])), "r"(__double2loint(v[14])), "r"(__double2hiint(v[14])), "r"(__double2loint(v[15])), "r"(__double2hiint(v[15])),
+                 "r"(__double2loint(v[16])), "r"(__double2hiint(v[16])), "r"(__double2loint(v[17])), "r"(__double2hiint(v[17])), "r"(__double2loint(v[18])), "r"(__double2hiint(v[18])), "r"(__double2loint(v[19])), "r"(__double2hiint(v[19])),
+                 "r"(__double2loint(v[20])), "r"(__double2hiint(v[20])), "r"(__double2loint(v[21])), "r"(__double2hiint(v[21])), "r"(__double2loint(v[22])), "r"(__double2hiint(v[22])), "r"(__double2loint(v[23])), "r"(__double2hiint(v[23])),
+                 "r"(__double2loint(v[24])), "r"(__double2hiint(v[24])), "r"(__double2loint(v[25])), "r"(__double2hiint(v[25])), "r"(__double2loint(v[26])), "r"(__double2hiint(v[26])), "r"(__double2loint(v[27])), "r"(__double2hiint(v[27])),
+                 "r"(__double2loint(v[28])), "r"(__double2hiint(v[28])), "r"(__double2loint(v[29])), "r"(__double2hiint(v[29])), "r"(__double2loint(v[30])), "r"(__double2hiint(v[30])), "r"(__double2loint(v[31])), "r"(__double2hiint(v[31])),
+                 "r"(ta) : "memory");
+}
+__device__ __forceinline__ void tmem_ld16x256(uint32_t ta, double* v) {     // 16 doubles, no wait
+  uint32_t u[32];
+  asm volatile("tcgen05.ld.sync.aligned.16x256b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
+               : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7]), "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]), "=r"(u[14]), "=r"(u[15]),
+                 "=r"(u[16]), "=r"(u[17]), "=r"(u[18]), "=r"(u[19]), "=r"(u[20]), "=r"(u[21]), "=r"(u[22]), "=r"(u[23]), "=r"(u[24]), "=r"(u[25]), "=r"(u[26]), "=r"(u[27]), "=r"(u[28]), "=r"(u[29]), "=r"(u[30]), "=r"(u[31])
+               : "r"(ta) : "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __hiloint2double(u[2 * i + 1], u[2 * i]);
+}
+// one trip of both planes: plane p at double columns [32 p, 32 p + 32) of this warp's TMEM slice
+__device__ __forceinline__ void tmem_trip2(uint32_t tm, double (&v)[2][32]) {
+  tmem_st32d(tm, v[0]);
+  tmem_st32d(tm + 64u, v[1]);
+  tmem_wait_st();
+  tmem_ld16x256(tm, v[0]);
+  tmem_ld16x256(tm + (16u << 16), v[0] + 16);
+  tmem_ld16x256(tm + 64u, v[1]);
+  tmem_ld16x256(tm + 64u + (16u << 16), v[1] + 16);
+  tmem_wait_ld();
+}
+template <int B>
+__device__ __forceinline__ void bfly_bit(double (&v)[32]) { bfly32<B, B + 1>(v); }
+__device__ __forceinline__ void transform10_tmem(uint32_t tm, double (&v)[2][32]) {
+  bfly32<0, 5>(v[0]); bfly32<0, 5>(v[1]);                 // e bits 5..9
+  tmem_trip2(tm, v);
+  bfly_bit<0>(v[0]); bfly_bit<4>(v[0]); bfly_bit<0>(v[1]); bfly_bit<4>(v[1]);   // e3, e4
+  tmem_trip2(tm, v);
+  bfly_bit<0>(v[0]); bfly_bit<4>(v[0]); bfly_bit<0>(v[1]); bfly_bit<4>(v[1]);   // e1, e2
+  tmem_trip2(tm, v);
+  bfly_bit<4>(v[0]); bfly_bit<4>(v[1]);                                           // e0
+}
+
 constexpr int PA10_NS = 4;                                   // staging ring depth
 constexpr int PA10_SMEM = PA10_NS * 2 * 1024 * 16 + 8 * padded(1024) * 8;  // 128 KB ring + 66 KB exchange
 
@@ -789,11 +888,18 @@ __global__ void __launch_bounds__(256, 1) k_passA10s(const typename Cx<V>::T* __
     bulk_g2s(dst, psi + (xh << 10), 1024 * sizeof(C2), &full[slot]);
     bulk_g2s(dst + 1024, psi + ((xh ^ (ag >> 10)) << 10), 1024 * sizeof(C2), &full[slot]);
   };
-  if (threadIdx.x == 0) {
+  constexpr bool TM = std::is_same<V, double>::value;           // FP64: transposes through TMEM
+  __shared__ uint32_t tmem_s;
+  if (TM && w == 0) tmem_alloc(&tmem_s, 256);
+  if (threadIdx.x == 32) {
     for (int i = 0; i < PA10_NS; ++i) { mbar_init(&full[i], 1); used[i] = 0; }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+  if (TM) tmem_fence_before();
   __syncthreads();
+  if (TM) tmem_fence_after();
+  // this warp's TMEM slice: its lane quadrant, double columns [0, 64) for w < 4, [64, 128) for w >= 4
+  const uint32_t tm = TM ? tmem_s + ((uint32_t)(32 * (w & 3)) << 16) + 128u * (uint32_t)(w >> 2) : 0u;
   if (threadIdx.x == 0)
     for (int i = 0; i < PA10_NS; ++i)
       if (blockIdx.x + (uint64_t)i * gridDim.x < items) issue(blockIdx.x + (uint64_t)i * gridDim.x, i);
@@ -829,7 +935,8 @@ __global__ void __launch_bounds__(256, 1) k_passA10s(const typename Cx<V>::T* __
       }
     }
     if (active) {
-      Rounds<10, 0, 0, 2, BarWarp, true, V>::run(v, xw, lane, BarWarp{});
+      if constexpr (TM) transform10_tmem(tm, v);              // position lane + 32 j <- pa10_freq
+      else Rounds<10, 0, 0, 2, BarWarp, true, V>::run(v, xw, lane, BarWarp{});
       // slab-major workspace: (y_h, pos) -> ((pos >> cb) << (H + cb)) | (y_h << cb) | (pos & (C-1))
       V* w0 = ws + (size_t)k * 2 * plane + (yh << cb);
       constexpr uint32_t cm = (1u << cb) - 1u;
@@ -841,6 +948,11 @@ __global__ void __launch_bounds__(256, 1) k_passA10s(const typename Cx<V>::T* __
         __stcg(w0 + plane + off, v[1][j]);
       }
     }
+  }
+  if constexpr (TM) {
+    tmem_fence_before();
+    __syncthreads();
+    if (w == 0) tmem_dealloc(tmem_s, 256);
   }
 }
 
@@ -918,8 +1030,8 @@ __global__ void __launch_bounds__(256, 1) k_passBt(int N, int kcount, const V* _
         for (int j = 0; j < 32; ++j) {
           const uint32_t e = lay(t, j, sf);
           const uint64_t pos = (slab << CB) | (e & ((1u << CB) - 1u));
-          // k_passA10s stores frequency b_l = 32 lane + j at pos = lane + 32 j (N <= 20)
-          const uint64_t bl = L == 10 ? (((pos & 31) << 5) | (pos >> 5)) : pos;
+          // k_passA10s (FP64, TMEM transposes) stores frequency pa10_freq(pos) at pos = lane + 32 j (N <= 20)
+          const uint64_t bl = L == 10 ? pa10_freq((uint32_t)pos) : pos;
           chi_store(al.chi, a, p, (int)(kp & 1), ((uint64_t)(e >> CB) << L) | bl, v[0][j]);
         }
       }
@@ -1039,43 +1151,6 @@ __global__ void __launch_bounds__(256, 1) k_passAs(const typename Cx<V>::T* __re
       __stcg(w0 + PLANE + off, v[1][j]);
     }
   }
-}
-
-// ------------------------------------------------------------------------------------------
-// Tensor memory (TMEM) as a per-thread register extension.  Thread lane of warp w owns TMEM
-// lane 32 (w % 4) + lane; a double occupies two consecutive 32-bit columns.  tcgen05.ld/st
-// run on the tensor-memory datapath, not on the L1TEX data pipe the transposes saturate.
-// ------------------------------------------------------------------------------------------
-__device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {   // one full warp
-  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n"
-               ::"r"(smem_u32(dst_smem)), "r"(ncols) : "memory");
-  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
-}
-__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {      // same warp
-  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(taddr), "r"(ncols) : "memory");
-}
-__device__ __forceinline__ void tmem_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
-__device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
-__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
-__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
-// 8 doubles -> columns [ta, ta + 16) of this thread's lane
-__device__ __forceinline__ void tmem_st8d(uint32_t ta, const double (&v)[8]) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%16], {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15};\n"
-               ::"r"(__double2loint(v[0])), "r"(__double2hiint(v[0])), "r"(__double2loint(v[1])), "r"(__double2hiint(v[1])),
-                 "r"(__double2loint(v[2])), "r"(__double2hiint(v[2])), "r"(__double2loint(v[3])), "r"(__double2hiint(v[3])),
-                 "r"(__double2loint(v[4])), "r"(__double2hiint(v[4])), "r"(__double2loint(v[5])), "r"(__double2hiint(v[5])),
-                 "r"(__double2loint(v[6])), "r"(__double2hiint(v[6])), "r"(__double2loint(v[7])), "r"(__double2hiint(v[7])),
-                 "r"(ta) : "memory");
-}
-// columns [ta, ta + 16) -> 8 doubles (no wait: the caller issues tmem_wait_ld before use)
-__device__ __forceinline__ void tmem_ld8d(uint32_t ta, uint32_t (&u)[16]) {
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];\n"
-               : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7]),
-                 "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]), "=r"(u[14]), "=r"(u[15])
-               : "r"(ta) : "memory");
-}
-__device__ __forceinline__ void stg_v4(double* p, double a, double b, double c, double d) {   // one 32-B sector
-  asm volatile("st.global.cg.v4.f64 [%0], {%1, %2, %3, %4};\n" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
 }
 
 // 64-point radix-2 butterflies over the register index (6 stages, pure DADD)
@@ -1341,8 +1416,8 @@ __global__ void __launch_bounds__(256, 1) k_passBr(int kcount, const double* __r
       for (int j = 0; j < 64; ++j) {
         const uint32_t e = tb | ((uint32_t)j << 1);
         const uint64_t pos = (slab << CB) | (e & ((1u << CB) - 1u));
-        // k_passAq: position = frequency; k_passA10s: frequency 32 lane + j sits at pos = lane + 32 j
-        const uint64_t bl = L == 10 ? (((pos & 31) << 5) | (pos >> 5)) : pos;
+        // k_passAq: position = frequency; k_passA10s: frequency pa10_freq(pos) sits at pos = lane + 32 j
+        const uint64_t bl = L == 10 ? pa10_freq((uint32_t)pos) : pos;
         chi_store(al.chi, a, p, (int)(kp & 1), ((uint64_t)(e >> CB) << L) | bl, v[j]);
       }
     }
