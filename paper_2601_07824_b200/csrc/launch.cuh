@@ -13,6 +13,8 @@
 #include <utility>
 #include <vector>
 
+#include <cudaTypedefs.h>
+
 #include "../../include/sre.h"
 #include "sre_kernels.cuh"
 
@@ -67,6 +69,7 @@ struct Plan {
   int KG = 0;               // 8-X-string groups per staged / streamed launch pair
   bool legacyA = false;     // SRE_LEGACY_A=1: round-1 three-round k_passAs for N = 21..24 (comparison)
   bool legacyB = false;     // SRE_LEGACY_B=1: round-1 three-round k_passBt<13, CB> for N = 21..24 (comparison)
+  bool rowmajor = false;    // FP64 N = 21..24: row-major workspace (k_passAw + TMA-gather k_passBw; SRE_SLAB=1: slab-major k_passAq + k_passBr)
 };
 
 // ------------------------------------------------------------------------------------------
@@ -248,10 +251,37 @@ cudaError_t launch_passAr_t(const Dev& d, const double2* psi, uint64_t a_first, 
   });
 }
 
+template <int N>
+cudaError_t launch_passAw_t(const Dev& d, const double2* psi, uint64_t a_first, int kcount, double* ws, cudaStream_t st) {
+  static const bool cs = [] { const char* e = getenv("SRE_PAW_CS"); return e && e[0] == '1'; }();
+  static uint64_t init_mask = 0, init_mask_cs = 0;
+  {
+    cudaError_t e = cs ? set_smem_once(k_passAw<N, true>, PAW_SMEM, init_mask_cs) : set_smem_once(k_passAw<N, false>, PAW_SMEM, init_mask);
+    if (e != cudaSuccess) return e;
+  }
+  const uint64_t groups = (uint64_t)(kcount + 3) / 4;
+  const uint64_t items = groups << (N - 13);                         // (row, group of 4 X-strings)
+  const unsigned grid = (unsigned)(items < (uint64_t)d.sms ? items : (uint64_t)d.sms);
+  const uint64_t gmagic = ((1ull << 40) + groups - 1) / groups;
+  return launch_counted(LK_PASSA, st, [&] {
+    if (cs) k_passAw<N, true><<<grid, 256, PAW_SMEM, st>>>(psi, a_first, kcount, gmagic, ws);
+    else k_passAw<N, false><<<grid, 256, PAW_SMEM, st>>>(psi, a_first, kcount, gmagic, ws);
+    return cudaGetLastError();
+  });
+}
+
 template <class V>
 cudaError_t launch_passA10s(const Plan& p, const Dev& d, const typename Cx<V>::T* psi, uint64_t a_first, int kcount,
                             V* ws, cudaStream_t st) {
   if constexpr (std::is_same<V, double>::value) {   // FP64 N = 21..24: radix-64 pass A (TMEM-parked plane B)
+    if (p.N >= 21 && p.N <= 24 && p.rowmajor) {
+      switch (p.N) {
+        case 21: return launch_passAw_t<21>(d, psi, a_first, kcount, ws, st);
+        case 22: return launch_passAw_t<22>(d, psi, a_first, kcount, ws, st);
+        case 23: return launch_passAw_t<23>(d, psi, a_first, kcount, ws, st);
+        case 24: return launch_passAw_t<24>(d, psi, a_first, kcount, ws, st);
+      }
+    }
     if (p.N >= 21 && p.N <= 24 && !p.legacyA) {
       switch (p.N) {
         case 21: return launch_passAr_t<21>(d, psi, a_first, kcount, ws, st);
@@ -306,10 +336,57 @@ cudaError_t launch_passBr_t(const Dev& d, int kcount, const double* ws, const Al
   });
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda at link time)
+inline PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+template <int CB, bool A2>
+cudaError_t launch_passBw_t(const Plan& p, const Dev& d, int kcount, const double* ws, const Alphas& al, double* partial,
+                            cudaStream_t st) {
+  static uint64_t init_mask = 0;
+  {
+    cudaError_t e = set_smem_once(k_passBw<CB, A2>, PBR_SMEM, init_mask);
+    if (e != cudaSuccess) return e;
+  }
+  constexpr int H = 13 - CB, R = H >= 8 ? 256 : (1 << H);
+  auto enc = tensor_map_encoder();
+  if (!enc) return cudaErrorNotSupported;
+  CUtensorMap tm;
+  const cuuint64_t dims[3] = {4096, 1ull << H, (cuuint64_t)2 * (cuuint64_t)kcount};
+  const cuuint64_t strides[2] = {4096 * sizeof(double), (1ull << (p.N - 1)) * sizeof(double)};
+  const cuuint32_t box[3] = {1u << CB, (cuuint32_t)R, 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(ws), dims, strides, box, es,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  return launch_counted(LK_PASSB, st, [&] {
+    k_passBw<CB, A2><<<d.sms, 256, PBR_SMEM, st>>>(kcount, tm, al, partial);
+    return cudaGetLastError();
+  });
+}
+
 template <class V, bool A2>
 cudaError_t launch_passBp(const Plan& p, const Dev& d, int kcount, const V* ws, const Alphas& al, double* partial,
                           cudaStream_t st) {
   if constexpr (std::is_same<V, double>::value) {   // FP64 N = 21..24: radix-64 pass B (one transpose)
+    if (p.N >= 21 && p.N <= 24 && p.rowmajor) {
+      switch (13 - p.H) {
+        case 5: return launch_passBw_t<5, A2>(p, d, kcount, ws, al, partial, st);
+        case 4: return launch_passBw_t<4, A2>(p, d, kcount, ws, al, partial, st);
+        case 3: return launch_passBw_t<3, A2>(p, d, kcount, ws, al, partial, st);
+        case 2: return launch_passBw_t<2, A2>(p, d, kcount, ws, al, partial, st);
+      }
+    }
     if (p.N >= 21 && p.N <= 24 && !p.legacyB) {
       switch (13 - p.H) {
         case 5: return launch_passBr_t<5, 12, A2>(d, kcount, ws, al, partial, st);

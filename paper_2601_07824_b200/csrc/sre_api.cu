@@ -168,6 +168,8 @@ int make_plan(int N, const Dev& d, Plan& p, uint64_t count = ~0ull) {
       p.legacyA = la && la[0] == '1';
       const char* lb = getenv("SRE_LEGACY_B");
       p.legacyB = lb && lb[0] == '1';
+      const char* sl = getenv("SRE_SLAB");
+      p.rowmajor = N <= 24 && !(sl && sl[0] == '1') && !p.legacyA && !p.legacyB;
     }
     if (p.L == 10) {  // staged pass A + persistent pass B (N = 15..20)
       p.staged = true;

@@ -19,6 +19,7 @@
 // round layout).
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <type_traits>
 
@@ -1418,6 +1419,254 @@ __global__ void __launch_bounds__(256, 1) k_passBr(int kcount, const double* __r
         const uint64_t pos = (slab << CB) | (e & ((1u << CB) - 1u));
         // k_passAq: position = frequency; k_passA10s: frequency pa10_freq(pos) sits at pos = lane + 32 j
         const uint64_t bl = L == 10 ? pa10_freq((uint32_t)pos) : pos;
+        chi_store(al.chi, a, p, (int)(kp & 1), ((uint64_t)(e >> CB) << L) | bl, v[j]);
+      }
+    }
+  }
+  block_flush(acc, partial, blockIdx.x);
+  if (al.hist) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < SPEC_BINS; i += blockDim.x)
+      if (shist[i]) atomicAdd(al.hist + i, shist[i]);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Row-major streamed path for N = 21..24 (FP64): k_passAw + k_passBw.
+// Workspace plane (X-string k, plane p) is row-major [2^H rows][4096 positions]: pass A writes each
+// 32 KB row contiguously (coalesced 16-B stores: HBM takes contiguous writes at ~6.3 TB/s against
+// 3.3-3.7 TB/s for the 32-B runs a slab-major layout forces, tools/microbench_wr.cu), and pass B
+// gathers a tile of 2^H rows x 2^CB columns with TMA tensor copies (32-B pieces at a 32 KB stride
+// read at 5.2 TB/s vs 7.3 for contiguous tiles) into the same smem layout k_passBr uses.
+// ------------------------------------------------------------------------------------------
+// k_passAw: CTA = 4 units x 64 threads; an item is (row y_h, group of 4 consecutive X-strings);
+// unit u takes X-string 4g + u.  The 4 X-strings share a_h and a_l >> 9, hence both psi rows and
+// every chunk: one ring of 16 KB stages (q chunk c, r chunk c ^ (a_l >> 9), 512 complex each) is
+// read by all 8 warps.  Radix-64 rounds as k_passAq; plane B parked in TMEM.  After round 1 the
+// unit stages its row in natural position order in its XOR-swizzled buffer and stores it with
+// coalesced 16-B stores.
+constexpr int PAW_NS = 4;                                             // ring stages (16 KB each)
+constexpr int PAW_SMEM = PAW_NS * 2 * 512 * 16 + 4 * 4096 * 8;        // 64 KB ring + 4 x 32 KB buffers
+
+template <int N, bool PAW_CS>
+__global__ void __launch_bounds__(256, 1) k_passAw(const double2* __restrict__ psi, uint64_t a_first, int kcount,
+                                                   uint64_t gmagic, double* __restrict__ ws) {
+  constexpr int L = 12, H = N - 1 - L;
+  static_assert(H >= 8 && H <= 11, "k_passAw covers N = 21..24");
+  constexpr uint64_t ROWS = 1ull << H;
+  constexpr size_t PLANE = (size_t)1 << (N - 1);
+  extern __shared__ __align__(128) double smem[];
+  double2* ring = reinterpret_cast<double2*>(smem);                 // [NS][q 512 | r 512]
+  double* exch = smem + PAW_NS * 2 * 512 * 2;                        // [unit][4096]
+  __shared__ __align__(8) uint64_t full[PAW_NS];
+  __shared__ int used[PAW_NS];
+  __shared__ uint32_t tmem_s;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int u = w >> 1;
+  const uint32_t t = threadIdx.x & 63;
+  const uint64_t groups = (uint64_t)(kcount + 3) / 4;
+  const uint64_t items = ROWS * groups;
+  const uint64_t my_items = items > blockIdx.x ? (items - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const uint64_t stages = my_items * 8;
+  auto split = [&](uint64_t item, uint64_t& yh, uint64_t& g) {       // gmagic = ceil(2^40 / groups)
+    yh = (item * gmagic) >> 40;
+    g = item - yh * groups;
+  };
+  if (w == 0) tmem_alloc(&tmem_s, 256);
+  if (threadIdx.x == 32) {
+    for (int i = 0; i < PAW_NS; ++i) { mbar_init(&full[i], 1); used[i] = 0; }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tm = tmem_s + ((uint32_t)(32 * (w & 3)) << 16) + 128u * (uint32_t)(w >> 2);
+  auto produce = [&](uint64_t s, int slot) {                       // one thread
+    uint64_t yh, g;
+    split(blockIdx.x + (s >> 3) * gridDim.x, yh, g);
+    const uint32_t c = (uint32_t)(s & 7);
+    const uint64_t a = a_first + 4 * g;
+    const int p = 63 - __clzll((long long)a);                       // >= 12
+    const uint64_t xh = ins0(yh, p - L);
+    const uint32_t ahi = (uint32_t)((a >> 9) & 7u);
+    double2* dst = ring + (size_t)slot * 1024;
+    mbar_expect_tx(&full[slot], 2 * 512 * sizeof(double2));
+    bulk_g2s(dst, psi + (xh << L) + 512 * c, 512 * sizeof(double2), &full[slot]);
+    bulk_g2s(dst + 512, psi + ((xh ^ (a >> L)) << L) + 512 * (c ^ ahi), 512 * sizeof(double2), &full[slot]);
+  };
+  if (threadIdx.x == 0)
+    for (int i = 0; i < PAW_NS; ++i)
+      if ((uint64_t)i < stages) produce(i, i);
+  double* xb = exch + (size_t)u * 4096;
+  const BarNamed bar{1 + u, 64};
+  uint64_t s = 0;
+  for (uint64_t li = 0; li < my_items; ++li) {
+    uint64_t yh, g;
+    split(blockIdx.x + li * gridDim.x, yh, g);
+    const int k = 4 * (int)g + u;
+    const bool active = k < kcount;
+    const uint32_t al = (uint32_t)((a_first + (uint64_t)k) & 4095u);
+    const uint32_t alo = al & 63u, ajh = (al >> 6) & 7u;
+    double v[64];
+#pragma unroll
+    for (int c = 0; c < 8; ++c, ++s) {
+      const int slot = (int)(s % PAW_NS);
+      mbar_wait(&full[slot], (uint32_t)(s / PAW_NS) & 1u);
+      const double2* cq = ring + (size_t)slot * 1024;
+      double b8[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const double2 q = cq[t + 64 * i];
+        const double2 r = cq[512 + (t ^ alo) + 64 * (i ^ ajh)];
+        v[8 * c + i] = fma(r.x, q.x, r.y * q.y);        // Re conj(psi_{x^a}) psi_x
+        b8[i] = fma(r.x, q.y, -(r.y * q.x));            // Im
+      }
+      if (active) tmem_st8d(tm + 16u * c, b8);
+      __syncwarp();
+      if (lane == 0) {                                   // release the stage; the 8th warp refills it
+        if (atomicAdd(&used[slot], 1) == 7) {
+          atomicExch(&used[slot], 0);
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          if (s + PAW_NS < stages) produce(s + PAW_NS, slot);
+        }
+      }
+    }
+    if (!active) continue;
+    tmem_wait_st();
+    double* wrow = ws + ((size_t)k * 2 << (N - 1)) + (yh << L);
+    auto transform_store = [&](double* wp) {
+      bfly64(v);                                         // round 0: pos bits 6..11
+      bar.sync();                                        // previous readers of xb are done
+#pragma unroll
+      for (int j = 0; j < 64; ++j) xb[xsw12(t + 64u * j)] = v[j];
+      bar.sync();
+#pragma unroll
+      for (int j = 0; j < 64; ++j) v[j] = xb[xsw12(64u * t + j)];
+      bar.sync();                                        // the transpose reads are done: reuse xb
+      bfly64(v);                                         // round 1: pos bits 0..5 (pos = 64 t + j)
+#pragma unroll
+      for (int j = 0; j < 64; ++j) xb[xsw12(64u * t + j)] = v[j];
+      bar.sync();
+      // chunk C = t + 64 i holds positions 2C, 2C + 1: one 16-B load (halves swapped when the XOR key
+      // flips bit 0) and one coalesced 16-B store -- each warp instruction writes 512 contiguous bytes
+#pragma unroll 8
+      for (int i = 0; i < 32; ++i) {
+        const uint32_t e = 2u * (t + 64u * i);
+        const uint32_t key = (e >> 6) & 15u;
+        const double2 x = *reinterpret_cast<const double2*>(xb + ((e ^ key) & ~1u));
+        const double2 y = (key & 1u) ? make_double2(x.y, x.x) : x;
+        if (PAW_CS) __stcs(reinterpret_cast<double2*>(wp + e), y);
+        else __stcg(reinterpret_cast<double2*>(wp + e), y);
+      }
+    };
+    transform_store(wrow);                               // plane A
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {                        // plane B back from TMEM
+      uint32_t r32[16];
+      tmem_ld8d(tm + 16u * c, r32);
+      tmem_wait_ld();
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[8 * c + i] = __hiloint2double(r32[2 * i + 1], r32[2 * i]);
+    }
+    transform_store(wrow + PLANE);                       // plane B
+  }
+  tmem_fence_before();
+  __syncthreads();
+  if (w == 0) tmem_dealloc(tmem_s, 256);
+}
+
+// TMA tensor copy of one box into shared memory, completing on an mbarrier
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tmap, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n"
+               ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// k_passBw: k_passBr's transform over the row-major planes of k_passAw.  Tile (plane kp = 2k + p,
+// column group s) = 2^H rows x 2^CB columns, gathered by 2^H / R TMA boxes of R = min(256, 2^H) rows
+// x 2^CB columns (tensor map: dims {4096, 2^H, 2K}) into the slot as e = row * 2^CB + col.
+template <int CB, bool A2>
+__global__ void __launch_bounds__(256, 1) k_passBw(int kcount, const __grid_constant__ CUtensorMap tmap, Alphas al,
+                                                   double* partial) {
+  ln_table_init(!A2 && al.need_log);   // t ln t pass (tile_accumulate)
+  constexpr int H = 13 - CB, L = 12;
+  static_assert(H >= 8 && H <= 11, "k_passBw covers N = 21..24");
+  constexpr int R = H >= 8 ? 256 : (1 << H), NBOX = (1 << H) / R;
+  extern __shared__ __align__(128) double smem[];
+  __shared__ __align__(8) uint64_t full[3];
+  __shared__ volatile unsigned long long issued[3];
+  __shared__ unsigned long long shist[SPEC_BINS];
+  const int u = threadIdx.x >> 7;
+  const uint32_t t = threadIdx.x & 127;
+  const uint64_t slabs = 1ull << (L - CB);
+  const uint64_t tiles = (uint64_t)kcount * 2 * slabs;
+  const uint64_t my_tiles = tiles > blockIdx.x ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const BarNamed bar{1 + u, 128};
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 3; ++i) { mbar_init(&full[i], 1); issued[i] = ~0ull; }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (al.hist)
+    for (int i = threadIdx.x; i < SPEC_BINS; i += blockDim.x) shist[i] = 0ull;
+  __syncthreads();
+  // issued[slot]: as in k_passBr (the two units share the three slots)
+  auto issue = [&](uint64_t n) {                                   // one thread
+    const int slot = (int)(n % 3);
+    issued[slot] = n;
+    const uint64_t tile = blockIdx.x + n * gridDim.x;
+    const int kp = (int)(tile / slabs), col = (int)(tile % slabs) << CB;
+    double* dst = smem + (size_t)slot * 8192;
+    mbar_expect_tx(&full[slot], 8192 * sizeof(double));
+#pragma unroll
+    for (int b = 0; b < NBOX; ++b) tma_load_3d(dst + b * (R << CB), &tmap, col, b * R, kp, &full[slot]);
+  };
+  if (threadIdx.x == 0)
+    for (uint64_t n = 0; n < 3 && n < my_tiles; ++n) issue(n);
+  double acc[NACC];
+#pragma unroll
+  for (int i = 0; i < NACC; ++i) acc[i] = 0.0;
+  for (uint64_t n = (uint64_t)u; n < my_tiles; n += 2) {
+    const int slot = (int)(n % 3);
+    double* buf = smem + (size_t)slot * 8192;
+    while (issued[slot] != n) __nanosleep(32);
+    mbar_wait(&full[slot], (uint32_t)(n / 3) & 1u);
+    double v[64];
+#pragma unroll
+    for (int j = 0; j < 64; ++j) v[j] = buf[t + 128u * j];      // round-0 layout, natural order
+    bfly64(v);                                                   // 6 high row bits
+    bar.sync();
+#pragma unroll
+    for (int j = 0; j < 64; ++j) buf[xsw13(t + 128u * j)] = v[j];
+    bar.sync();
+    const uint32_t tb = (t & 1u) | ((t >> 1) << 7);
+#pragma unroll
+    for (int j = 0; j < 64; ++j) v[j] = buf[xsw13(tb | ((uint32_t)j << 1))];
+    bar.sync();                                                  // slot free
+    if (t == 0) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      if (n + 3 < my_tiles) issue(n + 3);
+    }
+    constexpr int CLO = CB - 1;
+#pragma unroll
+    for (int h = 1 << CLO; h < 64; h <<= 1)
+#pragma unroll
+      for (int i = 0; i < 64; ++i) {
+        if (i & h) continue;
+        const double a = v[i], b = v[i + h];
+        v[i] = a + b;
+        v[i + h] = a - b;
+      }
+    tile_accumulate<A2>(acc, v, al);
+    if (al.hist) spec_add(shist, v);
+    if (al.chi) {     // sre_chi: tile element e = (row, col) of column group slab -> b' = (row << L) | position
+      const uint64_t tile = blockIdx.x + n * gridDim.x;
+      const uint64_t kp = tile / slabs, slab = tile % slabs;
+      const uint64_t a = al.chi_a0 + (kp >> 1);
+      const int p = pivot_of(a, L + H + 1);
+#pragma unroll
+      for (int j = 0; j < 64; ++j) {
+        const uint32_t e = tb | ((uint32_t)j << 1);
+        const uint64_t bl = (slab << CB) | (e & ((1u << CB) - 1u));
         chi_store(al.chi, a, p, (int)(kp & 1), ((uint64_t)(e >> CB) << L) | bl, v[j]);
       }
     }

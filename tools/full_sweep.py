@@ -29,6 +29,7 @@ from bench import Clocks, load_peaks  # noqa: E402
 n = int(sys.argv[1])
 kind = sys.argv[2]
 chunk = 1 << (int(sys.argv[3]) if len(sys.argv) > 3 else 19)
+max_chunks = int(sys.argv[4]) if len(sys.argv) > 4 else None     # timing slices only (no pin)
 alphas = [2.0]
 t0 = time.time()
 if kind == "scrambled":
@@ -48,6 +49,8 @@ chunk_ms = []
 clk = Clocks(0)
 wall0 = time.perf_counter()
 for a in range(0, D, chunk):
+    if max_chunks is not None and len(chunk_ms) >= max_chunks:
+        break
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     sre.partial_sums(psi, a, min(D, a + chunk), alphas, out=out, workspace=ws)
@@ -60,6 +63,13 @@ wall = time.perf_counter() - wall0
 clocks = clk.stop()
 m, ln = sre.finalize(acc.reshape(1, 3), n, alphas)
 dev_s = sum(chunk_ms) / 1e3
+swept = min(D, len(chunk_ms) * chunk)
+if swept < D:                                  # a timing slice: rates over the X-strings swept
+    print(json.dumps({"N": n, "state": kind, "x_strings": swept, "device_seconds": dev_s,
+                      "us_per_x_string": dev_s / swept * 1e6, "pauli_per_s": swept * 2.0 ** n / dev_s,
+                      "frac_of_hbm": 16.0 * swept * 2.0 ** n / dev_s / 1e9 / load_peaks()[0]["hbm_gbs"],
+                      "clocks": clocks}), flush=True)
+    sys.exit(0)
 peaks, psrc = load_peaks()
 line = {
     "N": n, "state": kind, "alpha": alphas, "M2": float(m[0][0]), "lost_norm": float(ln[0]),

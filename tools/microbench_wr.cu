@@ -58,6 +58,21 @@ __global__ void __launch_bounds__(256, 1) k_wr(double* ws, int K) {
       }
       continue;
     }
+    if (MODE == 9) {                                       // CB = 3 slabs (2^11 rows x 8 cols): 4 rows per CTA, 64-B row runs
+      const uint64_t rb = it / K, kk = it % K;
+      const uint64_t yh9 = rb * 4 + u;
+      for (int pl = 0; pl < 2; ++pl) {
+        double* wp = ws + (size_t)kk * 2 * PLANE + (size_t)pl * PLANE;
+#pragma unroll
+        for (int r4 = 0; r4 < 16; ++r4) {
+          const uint32_t pos = 64u * t + 4u * r4;
+          const size_t off = ((size_t)(pos >> 3) << (H + 3)) + (yh9 << 3) + (pos & 7u);
+          const double v = (double)(pos + yh9);
+          stg_v4(wp + off, v, v + 1, v + 2, v + 3);
+        }
+      }
+      continue;
+    }
     if (MODE == 1) {                                       // 4 consecutive rows of one X-string
       const uint64_t rb = it / K, kk = it % K;             // row block of 4, X-string
       yh = rb * 4 + u; k = kk;
@@ -91,7 +106,8 @@ __global__ void __launch_bounds__(256) k_rd(const double* __restrict__ ws, uint6
     const double* base;
     size_t stride;
     if (RMODE == 0) { base = ws + tile * 8192; stride = 4; }
-    else { base = ws + (tile >> 2) * 32768 + 4 * (tile & 3); stride = 16; }
+    else if (RMODE == 1) { base = ws + (tile >> 2) * 32768 + 4 * (tile & 3); stride = 16; }
+    else { base = ws + (tile >> 10) * (8192ull * 1024) + 4 * (tile & 1023); stride = 4096; }   // row-major [2048][4096] planes
     for (int r = threadIdx.x; r < 2048; r += 256) {
       double a, b, c, d;
       asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(base + r * stride));
@@ -174,11 +190,12 @@ int main() {
     run(k_wr<5>, "slab32B_16rows_512B_runs", K);
     run(k_wr<6>, "coalesced_contiguous", K);
     run(k_wrc<7>, "cluster4_synced_4row_lines", K);
+    run(k_wr<9>, "slab64B_4rows_per_cta", K);
     run(k_wr8, "slab32B_8rows_256B_runs", K);
   }
-  for (int rm = 0; rm < 2; ++rm) {
+  for (int rm = 0; rm < 3; ++rm) {
     const uint64_t tiles = bytes / 8 / 8192;
-    auto kern = rm == 0 ? k_rd<0> : k_rd<1>;
+    auto kern = rm == 0 ? k_rd<0> : rm == 1 ? k_rd<1> : k_rd<2>;
     kern<<<4 * sms, 256>>>(ws, tiles, ws);
     cudaEventRecord(e0);
     for (int i = 0; i < 3; ++i) kern<<<4 * sms, 256>>>(ws, tiles, ws);
