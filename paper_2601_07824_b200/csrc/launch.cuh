@@ -201,19 +201,19 @@ cudaError_t launch_passB(const Plan& p, uint64_t a0, int kcount, const V* ws, co
   return cudaErrorInvalidValue;
 }
 
-template <class V, int N>
+template <class V, int N, bool ROWM = false>
 cudaError_t launch_passA10s_t(const Dev& d, const typename Cx<V>::T* psi, uint64_t a_first, int kcount, V* ws,
                               cudaStream_t st) {
   static uint64_t init_mask = 0;   // per device: the attribute belongs to the device context
   {
-    cudaError_t e = set_smem_once(k_passA10s<N, V>, PA10_SMEM, init_mask);
+    cudaError_t e = set_smem_once(k_passA10s<N, V, ROWM>, PA10_SMEM, init_mask);
     if (e != cudaSuccess) return e;
   }
   const int groups = (kcount + 7) / 8;
   const uint64_t items = (uint64_t)groups << (N - 11);
   const unsigned grid = (unsigned)(items < (uint64_t)d.sms ? items : (uint64_t)d.sms);
   return launch_counted(LK_PASSA, st, [&] {
-    k_passA10s<N, V><<<grid, 256, PA10_SMEM, st>>>(psi, a_first, kcount, groups, ws);
+    k_passA10s<N, V, ROWM><<<grid, 256, PA10_SMEM, st>>>(psi, a_first, kcount, groups, ws);
     return cudaGetLastError();
   });
 }
@@ -273,6 +273,7 @@ cudaError_t launch_passAw_t(const Dev& d, const double2* psi, uint64_t a_first, 
 template <class V>
 cudaError_t launch_passA10s(const Plan& p, const Dev& d, const typename Cx<V>::T* psi, uint64_t a_first, int kcount,
                             V* ws, cudaStream_t st) {
+  constexpr bool F64 = std::is_same<V, double>::value;
   if constexpr (std::is_same<V, double>::value) {   // FP64 N = 21..24: radix-64 pass A (TMEM-parked plane B)
     if (p.N >= 21 && p.N <= 24 && p.rowmajor) {
       switch (p.N) {
@@ -297,12 +298,16 @@ cudaError_t launch_passA10s(const Plan& p, const Dev& d, const typename Cx<V>::T
     case 23: return launch_passAs_t<V, 23, 12>(d, psi, a_first, kcount, ws, st);
     case 24: return launch_passAs_t<V, 24, 12>(d, psi, a_first, kcount, ws, st);
     case 25: return launch_passAs_t<V, 25, 13>(d, psi, a_first, kcount, ws, st);
-    case 15: return launch_passA10s_t<V, 15>(d, psi, a_first, kcount, ws, st);
+    case 15: return launch_passA10s_t<V, 15>(d, psi, a_first, kcount, ws, st);   // FP32: slab-major (k_passBt)
     case 16: return launch_passA10s_t<V, 16>(d, psi, a_first, kcount, ws, st);
-    case 17: return launch_passA10s_t<V, 17>(d, psi, a_first, kcount, ws, st);
-    case 18: return launch_passA10s_t<V, 18>(d, psi, a_first, kcount, ws, st);
-    case 19: return launch_passA10s_t<V, 19>(d, psi, a_first, kcount, ws, st);
-    case 20: return launch_passA10s_t<V, 20>(d, psi, a_first, kcount, ws, st);
+    case 17: return p.rowmajor && F64 ? launch_passA10s_t<V, 17, F64>(d, psi, a_first, kcount, ws, st)
+                               : launch_passA10s_t<V, 17>(d, psi, a_first, kcount, ws, st);
+    case 18: return p.rowmajor && F64 ? launch_passA10s_t<V, 18, F64>(d, psi, a_first, kcount, ws, st)
+                               : launch_passA10s_t<V, 18>(d, psi, a_first, kcount, ws, st);
+    case 19: return p.rowmajor && F64 ? launch_passA10s_t<V, 19, F64>(d, psi, a_first, kcount, ws, st)
+                               : launch_passA10s_t<V, 19>(d, psi, a_first, kcount, ws, st);
+    case 20: return p.rowmajor && F64 ? launch_passA10s_t<V, 20, F64>(d, psi, a_first, kcount, ws, st)
+                               : launch_passA10s_t<V, 20>(d, psi, a_first, kcount, ws, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -349,20 +354,20 @@ inline PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return fn;
 }
 
-template <int CB, bool A2>
+template <int CB, int L, bool A2>
 cudaError_t launch_passBw_t(const Plan& p, const Dev& d, int kcount, const double* ws, const Alphas& al, double* partial,
                             cudaStream_t st) {
   static uint64_t init_mask = 0;
   {
-    cudaError_t e = set_smem_once(k_passBw<CB, A2>, PBR_SMEM, init_mask);
+    cudaError_t e = set_smem_once(k_passBw<CB, L, A2>, PBR_SMEM, init_mask);
     if (e != cudaSuccess) return e;
   }
   constexpr int H = 13 - CB, R = H >= 8 ? 256 : (1 << H);
   auto enc = tensor_map_encoder();
   if (!enc) return cudaErrorNotSupported;
   CUtensorMap tm;
-  const cuuint64_t dims[3] = {4096, 1ull << H, (cuuint64_t)2 * (cuuint64_t)kcount};
-  const cuuint64_t strides[2] = {4096 * sizeof(double), (1ull << (p.N - 1)) * sizeof(double)};
+  const cuuint64_t dims[3] = {1ull << L, 1ull << H, (cuuint64_t)2 * (cuuint64_t)kcount};
+  const cuuint64_t strides[2] = {(1ull << L) * sizeof(double), (1ull << (p.N - 1)) * sizeof(double)};
   const cuuint32_t box[3] = {1u << CB, (cuuint32_t)R, 1};
   const cuuint32_t es[3] = {1, 1, 1};
   if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(ws), dims, strides, box, es,
@@ -370,7 +375,7 @@ cudaError_t launch_passBw_t(const Plan& p, const Dev& d, int kcount, const doubl
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
   return launch_counted(LK_PASSB, st, [&] {
-    k_passBw<CB, A2><<<d.sms, 256, PBR_SMEM, st>>>(kcount, tm, al, partial);
+    k_passBw<CB, L, A2><<<d.sms, 256, PBR_SMEM, st>>>(kcount, tm, al, partial);
     return cudaGetLastError();
   });
 }
@@ -381,10 +386,10 @@ cudaError_t launch_passBp(const Plan& p, const Dev& d, int kcount, const V* ws, 
   if constexpr (std::is_same<V, double>::value) {   // FP64 N = 21..24: radix-64 pass B (one transpose)
     if (p.N >= 21 && p.N <= 24 && p.rowmajor) {
       switch (13 - p.H) {
-        case 5: return launch_passBw_t<5, A2>(p, d, kcount, ws, al, partial, st);
-        case 4: return launch_passBw_t<4, A2>(p, d, kcount, ws, al, partial, st);
-        case 3: return launch_passBw_t<3, A2>(p, d, kcount, ws, al, partial, st);
-        case 2: return launch_passBw_t<2, A2>(p, d, kcount, ws, al, partial, st);
+        case 5: return launch_passBw_t<5, 12, A2>(p, d, kcount, ws, al, partial, st);
+        case 4: return launch_passBw_t<4, 12, A2>(p, d, kcount, ws, al, partial, st);
+        case 3: return launch_passBw_t<3, 12, A2>(p, d, kcount, ws, al, partial, st);
+        case 2: return launch_passBw_t<2, 12, A2>(p, d, kcount, ws, al, partial, st);
       }
     }
     if (p.N >= 21 && p.N <= 24 && !p.legacyB) {
@@ -393,6 +398,14 @@ cudaError_t launch_passBp(const Plan& p, const Dev& d, int kcount, const V* ws, 
         case 4: return launch_passBr_t<4, 12, A2>(d, kcount, ws, al, partial, st);
         case 3: return launch_passBr_t<3, 12, A2>(d, kcount, ws, al, partial, st);
         case 2: return launch_passBr_t<2, 12, A2>(d, kcount, ws, al, partial, st);
+      }
+    }
+    if (p.N >= 17 && p.N <= 20 && p.rowmajor) {   // k_passA10s<ROWM> wrote row-major planes
+      switch (13 - p.H) {
+        case 7: return launch_passBw_t<7, 10, A2>(p, d, kcount, ws, al, partial, st);
+        case 6: return launch_passBw_t<6, 10, A2>(p, d, kcount, ws, al, partial, st);
+        case 5: return launch_passBw_t<5, 10, A2>(p, d, kcount, ws, al, partial, st);
+        case 4: return launch_passBw_t<4, 10, A2>(p, d, kcount, ws, al, partial, st);
       }
     }
     if (p.N >= 17 && p.N <= 20) {   // k_passA10s wrote 2^13-double tiles for these (its cb = 13 - H)

@@ -862,7 +862,7 @@ constexpr int PA10_SMEM = PA10_NS * 2 * 1024 * 16 + 8 * padded(1024) * 8;  // 12
 // finish with a ring slot refills it with the item NS positions ahead.  Warp w generates
 // X-string 8g + w from the staged rows, transforms 10 bits (one warp-local exchange per
 // plane) and writes its row of both planes.
-template <int N, class V = double>
+template <int N, class V = double, bool ROWM = false>   // ROWM: row-major planes [2^H][1024] (FP64, k_passBw)
 __global__ void __launch_bounds__(256, 1) k_passA10s(const typename Cx<V>::T* __restrict__ psi, uint64_t a_first,
                                                      int kcount, int groups, V* __restrict__ ws) {
   using C2 = typename Cx<V>::T;
@@ -938,6 +938,15 @@ __global__ void __launch_bounds__(256, 1) k_passA10s(const typename Cx<V>::T* __
     if (active) {
       if constexpr (TM) transform10_tmem(tm, v);              // position lane + 32 j <- pa10_freq
       else Rounds<10, 0, 0, 2, BarWarp, true, V>::run(v, xw, lane, BarWarp{});
+      if constexpr (ROWM) {                                     // row-major: 8 KB per row, 256 B per store
+        V* w0 = ws + (size_t)k * 2 * plane + (yh << 10) + lane;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          __stcg(w0 + 32 * j, v[0][j]);
+          __stcg(w0 + plane + 32 * j, v[1][j]);
+        }
+        continue;
+      }
       // slab-major workspace: (y_h, pos) -> ((pos >> cb) << (H + cb)) | (y_h << cb) | (pos & (C-1))
       V* w0 = ws + (size_t)k * 2 * plane + (yh << cb);
       constexpr uint32_t cm = (1u << cb) - 1u;
@@ -1582,15 +1591,16 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tmap, 
                : "memory");
 }
 
-// k_passBw: k_passBr's transform over the row-major planes of k_passAw.  Tile (plane kp = 2k + p,
-// column group s) = 2^H rows x 2^CB columns, gathered by 2^H / R TMA boxes of R = min(256, 2^H) rows
-// x 2^CB columns (tensor map: dims {4096, 2^H, 2K}) into the slot as e = row * 2^CB + col.
-template <int CB, bool A2>
+// k_passBw: k_passBr's transform over the row-major planes of k_passAw (L = 12) or k_passA10s<ROWM>
+// (L = 10).  Tile (plane kp = 2k + p, column group s) = 2^H rows x 2^CB columns, gathered by 2^H / R
+// TMA boxes of R = min(256, 2^H) rows x 2^CB columns (tensor map: dims {2^L, 2^H, 2K}) into the slot
+// as e = row * 2^CB + col.
+template <int CB, int L, bool A2>
 __global__ void __launch_bounds__(256, 1) k_passBw(int kcount, const __grid_constant__ CUtensorMap tmap, Alphas al,
                                                    double* partial) {
   ln_table_init(!A2 && al.need_log);   // t ln t pass (tile_accumulate)
-  constexpr int H = 13 - CB, L = 12;
-  static_assert(H >= 8 && H <= 11, "k_passBw covers N = 21..24");
+  constexpr int H = 13 - CB;
+  static_assert(H >= 6 && H <= 11, "k_passBw: N = 17..20 (L = 10) and 21..24 (L = 12)");
   constexpr int R = H >= 8 ? 256 : (1 << H), NBOX = (1 << H) / R;
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t full[3];
@@ -1666,7 +1676,8 @@ __global__ void __launch_bounds__(256, 1) k_passBw(int kcount, const __grid_cons
 #pragma unroll
       for (int j = 0; j < 64; ++j) {
         const uint32_t e = tb | ((uint32_t)j << 1);
-        const uint64_t bl = (slab << CB) | (e & ((1u << CB) - 1u));
+        const uint64_t pos = (slab << CB) | (e & ((1u << CB) - 1u));
+        const uint64_t bl = L == 10 ? pa10_freq((uint32_t)pos) : pos;   // k_passA10s: TMEM-transposed order
         chi_store(al.chi, a, p, (int)(kp & 1), ((uint64_t)(e >> CB) << L) | bl, v[j]);
       }
     }

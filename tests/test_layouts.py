@@ -1,0 +1,88 @@
+"""Index algebra of the sm_100a kernels, checked on the CPU (no GPU): the TMEM transpose trips of
+k_passA10s, the XOR swizzles of the radix-64 transposes, and their shared-memory bank behaviour.
+The GPU tests (element-wise chi through the production kernels) check the same maps on hardware."""
+
+
+def trip(state):
+    """tcgen05.st 32x32b (thread l -> lane l, double column r) then two tcgen05.ld 16x256b.x8 at lane
+    bases 0/16: thread t = t0 + 4 t1 gets lane 16b + 8s + t1, column 4c + t0 into register
+    r = s + 2c + 16b (CUTLASS Copy_Traits<SM100_TMEM_LOAD_16dp256b1x>::DstLayout)."""
+    new = [[None] * 32 for _ in range(32)]
+    for t in range(32):
+        t0, t1 = t & 3, t >> 2
+        for b in range(2):
+            for c in range(8):
+                for s in range(2):
+                    new[t][s + 2 * c + 16 * b] = state[16 * b + 8 * s + t1][4 * c + t0]
+    return new
+
+
+def pa10_freq(pos):          # csrc/sre_kernels.cuh, written out again
+    t, r = pos & 31, pos >> 5
+    bits = [(t & 1, 1), ((t >> 1) & 1, 8), ((t >> 2) & 1, 3), ((t >> 3) & 1, 7), ((t >> 4) & 1, 5),
+            (r & 1, 6), ((r >> 1) & 1, 9), ((r >> 2) & 1, 4), ((r >> 3) & 1, 2), ((r >> 4) & 1, 0)]
+    return sum(v << k for v, k in bits)
+
+
+def test_tmem_trips_cover_every_bit_and_match_pa10_freq():
+    state = [[l + 32 * j for j in range(32)] for l in range(32)]   # element e = lane + 32 j
+    butterflied = {5, 6, 7, 8, 9}                                     # round 0: register bits
+    schedule = [(0, 4), (0, 4), (4,)]                                 # register bits butterflied per trip
+    for regbits in schedule:
+        state = trip(state)
+        for rb in regbits:   # the register bit rb must flip exactly one element bit, not yet done
+            diff = state[0][1 << rb] ^ state[0][0]
+            assert diff & (diff - 1) == 0
+            k = diff.bit_length() - 1
+            assert k not in butterflied
+            butterflied.add(k)
+            assert all((state[t][r] ^ state[t][r ^ (1 << rb)]) == diff for t in range(32) for r in range(32))
+    assert butterflied == set(range(10))
+    for t in range(32):
+        for r in range(32):
+            assert state[t][r] == pa10_freq(t + 32 * r)
+    assert sorted(pa10_freq(p) for p in range(1024)) == list(range(1024))
+
+
+def xsw12(e):
+    return e ^ ((e >> 6) & 15)
+
+
+def xsw13(e):
+    return e ^ (((e >> 7) & 7) << 1)
+
+
+def _half_warp_conflict_free(addrs):          # 8-B accesses: 16 lanes of a half-warp, 16 double banks
+    return all(len({a % 16 for a in addrs[h:h + 16]}) == 16 for h in (0, 16))
+
+
+def test_radix64_swizzles_bijective_and_conflict_free():
+    assert sorted(map(xsw12, range(4096))) == list(range(4096))
+    assert sorted(map(xsw13, range(8192))) == list(range(8192))
+    # k_passAq / k_passAw: unit of 64 threads, thread t = 32 w + lane; round 0 STS at t + 64 j,
+    # round 1 LDS at 64 t + j
+    for w in range(2):
+        for j in range(64):
+            assert _half_warp_conflict_free([xsw12(32 * w + l + 64 * j) for l in range(32)])
+            assert _half_warp_conflict_free([xsw12(64 * (32 * w + l) + j) for l in range(32)])
+    # k_passBr / k_passBw: 128 threads; round 0 STS at t + 128 j, round 1 LDS at tb | (j << 1) with
+    # tb = (t & 1) | ((t >> 1) << 7)
+    for w in range(4):
+        for j in range(64):
+            ts = [32 * w + l for l in range(32)]
+            assert _half_warp_conflict_free([xsw13(t + 128 * j) for t in ts])
+            assert _half_warp_conflict_free([xsw13((t & 1) | ((t >> 1) << 7) | (j << 1)) for t in ts])
+
+
+def test_row_staging_reads_pairs():
+    """k_passAw stages a row at xsw12(pos) and reads 16-B chunks C = t + 64 i as the pair (2C, 2C+1):
+    both sit in one aligned 16-B slot (swapped when the XOR key is odd), and a quarter-warp's 8
+    chunks hit 8 distinct 16-B bank groups."""
+    for c in range(2048):
+        e = 2 * c
+        key = (e >> 6) & 15
+        base = (e ^ key) & ~1
+        got = (base, base + 1) if key % 2 == 0 else (base + 1, base)
+        assert (xsw12(e), xsw12(e + 1)) == got
+    for q in range(0, 2048, 8):
+        assert len({((2 * c) ^ ((2 * c >> 6) & 15)) // 2 % 8 for c in range(q, q + 8)}) == 8
