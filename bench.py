@@ -56,9 +56,9 @@ FP64_OPS_PER_CLK_SM = 64        # B200 FP64 pipe (measured 63.9/clk/SM, profiles
 
 def ncu_traffic(config, kind):
     """roofline.traffic: DRAM bytes per launch of the dominant kernel from the committed `ncu --set full`
-    capture of this config (profiles/r01_traffic.json, written by tools/ncu_traffic.py), else None."""
+    capture of this config (profiles/r02_traffic.json, written by tools/ncu_traffic.py), else None."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r02_traffic.json")) as f:
             t = json.load(f).get(config)
     except (OSError, ValueError):
         return None

@@ -35,7 +35,7 @@ def test_ncu_traffic_reducer(tmp_path, monkeypatch):
 def test_bench_traffic_lookup():
     bench = _load("bench_mod", "bench.py")
     assert bench.ncu_traffic("no-such-config", "pass_a") is None
-    path = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    path = os.path.join(ROOT, "profiles", "r02_traffic.json")
     if os.path.exists(path):
         for cfg, t in json.load(open(path)).items():
             assert t["kind"] in ("pass_a", "pass_b", "single_pass")

@@ -2,7 +2,7 @@
 
 Runs the short configs (c3: 256 x N=14 states; x8: N_A=8 mixed mana) for one timed step; the
 roofline must name a kernel that launched, and traffic must come from the committed ncu capture
-when one exists for the config (profiles/r01_traffic.json)."""
+when one exists for the config (profiles/r02_traffic.json)."""
 import json
 import os
 import subprocess
@@ -38,7 +38,7 @@ def test_bench_line_contract(config):
     assert r["launches_timed"] > 0 and r["avg_launch_ms"] > 0
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
-    path = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    path = os.path.join(ROOT, "profiles", "r02_traffic.json")
     t = json.load(open(path)).get(config) if os.path.exists(path) else None
     if t and t["kind"] == r["kernel"]:
         assert r["traffic"] == t["dram_bytes_per_launch"]
