@@ -67,9 +67,6 @@ struct Plan {
   bool staged = false;      // staged (N = 15..20) or streamed (N = 21..25) pass A + TMA-fed pass B
   uint64_t amin = 0;        // first X-string the staged / streamed kernels accept (a_h != 0)
   int KG = 0;               // 8-X-string groups per staged / streamed launch pair
-  bool legacyA = false;     // SRE_LEGACY_A=1: round-1 three-round k_passAs for N = 21..24 (comparison)
-  bool legacyB = false;     // SRE_LEGACY_B=1: round-1 three-round k_passBt<13, CB> for N = 21..24 (comparison)
-  bool rowmajor = false;    // FP64 N = 21..24: row-major workspace (k_passAw + TMA-gather k_passBw; SRE_SLAB=1: slab-major k_passAq + k_passBr)
 };
 
 // ------------------------------------------------------------------------------------------
@@ -236,22 +233,6 @@ cudaError_t launch_passAs_t(const Dev& d, const typename Cx<V>::T* psi, uint64_t
 }
 
 template <int N>
-cudaError_t launch_passAr_t(const Dev& d, const double2* psi, uint64_t a_first, int kcount, double* ws, cudaStream_t st) {
-  static uint64_t init_mask = 0;   // per device: the attribute belongs to the device context
-  {
-    cudaError_t e = set_smem_once(k_passAq<N>, PAQ_SMEM, init_mask);
-    if (e != cudaSuccess) return e;
-  }
-  const uint64_t items = (uint64_t)kcount << (N - 15);               // (4-row block, X-string)
-  const unsigned grid = (unsigned)(items < (uint64_t)d.sms ? items : (uint64_t)d.sms);
-  const uint64_t kmagic = ((1ull << 40) + (uint64_t)kcount - 1) / (uint64_t)kcount;
-  return launch_counted(LK_PASSA, st, [&] {
-    k_passAq<N><<<grid, 256, PAQ_SMEM, st>>>(psi, a_first, kcount, kmagic, ws);
-    return cudaGetLastError();
-  });
-}
-
-template <int N>
 cudaError_t launch_passAw_t(const Dev& d, const double2* psi, uint64_t a_first, int kcount, double* ws, cudaStream_t st) {
   static const bool cs = [] { const char* e = getenv("SRE_PAW_CS"); return e && e[0] == '1'; }();
   static uint64_t init_mask = 0, init_mask_cs = 0;
@@ -273,22 +254,14 @@ cudaError_t launch_passAw_t(const Dev& d, const double2* psi, uint64_t a_first, 
 template <class V>
 cudaError_t launch_passA10s(const Plan& p, const Dev& d, const typename Cx<V>::T* psi, uint64_t a_first, int kcount,
                             V* ws, cudaStream_t st) {
-  constexpr bool F64 = std::is_same<V, double>::value;
-  if constexpr (std::is_same<V, double>::value) {   // FP64 N = 21..24: radix-64 pass A (TMEM-parked plane B)
-    if (p.N >= 21 && p.N <= 24 && p.rowmajor) {
+  constexpr bool F64 = std::is_same<V, double>::value;   // FP64 N >= 17: row-major workspace planes
+  if constexpr (F64) {   // FP64 N = 21..24: radix-64 pass A (TMEM-parked plane B), row-major rows
+    if (p.N >= 21 && p.N <= 24) {
       switch (p.N) {
         case 21: return launch_passAw_t<21>(d, psi, a_first, kcount, ws, st);
         case 22: return launch_passAw_t<22>(d, psi, a_first, kcount, ws, st);
         case 23: return launch_passAw_t<23>(d, psi, a_first, kcount, ws, st);
         case 24: return launch_passAw_t<24>(d, psi, a_first, kcount, ws, st);
-      }
-    }
-    if (p.N >= 21 && p.N <= 24 && !p.legacyA) {
-      switch (p.N) {
-        case 21: return launch_passAr_t<21>(d, psi, a_first, kcount, ws, st);
-        case 22: return launch_passAr_t<22>(d, psi, a_first, kcount, ws, st);
-        case 23: return launch_passAr_t<23>(d, psi, a_first, kcount, ws, st);
-        case 24: return launch_passAr_t<24>(d, psi, a_first, kcount, ws, st);
       }
     }
   }
@@ -298,16 +271,12 @@ cudaError_t launch_passA10s(const Plan& p, const Dev& d, const typename Cx<V>::T
     case 23: return launch_passAs_t<V, 23, 12>(d, psi, a_first, kcount, ws, st);
     case 24: return launch_passAs_t<V, 24, 12>(d, psi, a_first, kcount, ws, st);
     case 25: return launch_passAs_t<V, 25, 13>(d, psi, a_first, kcount, ws, st);
-    case 15: return launch_passA10s_t<V, 15>(d, psi, a_first, kcount, ws, st);   // FP32: slab-major (k_passBt)
+    case 15: return launch_passA10s_t<V, 15>(d, psi, a_first, kcount, ws, st);   // slab-major tiles for k_passBt
     case 16: return launch_passA10s_t<V, 16>(d, psi, a_first, kcount, ws, st);
-    case 17: return p.rowmajor && F64 ? launch_passA10s_t<V, 17, F64>(d, psi, a_first, kcount, ws, st)
-                               : launch_passA10s_t<V, 17>(d, psi, a_first, kcount, ws, st);
-    case 18: return p.rowmajor && F64 ? launch_passA10s_t<V, 18, F64>(d, psi, a_first, kcount, ws, st)
-                               : launch_passA10s_t<V, 18>(d, psi, a_first, kcount, ws, st);
-    case 19: return p.rowmajor && F64 ? launch_passA10s_t<V, 19, F64>(d, psi, a_first, kcount, ws, st)
-                               : launch_passA10s_t<V, 19>(d, psi, a_first, kcount, ws, st);
-    case 20: return p.rowmajor && F64 ? launch_passA10s_t<V, 20, F64>(d, psi, a_first, kcount, ws, st)
-                               : launch_passA10s_t<V, 20>(d, psi, a_first, kcount, ws, st);
+    case 17: return launch_passA10s_t<V, 17, F64>(d, psi, a_first, kcount, ws, st);
+    case 18: return launch_passA10s_t<V, 18, F64>(d, psi, a_first, kcount, ws, st);
+    case 19: return launch_passA10s_t<V, 19, F64>(d, psi, a_first, kcount, ws, st);
+    case 20: return launch_passA10s_t<V, 20, F64>(d, psi, a_first, kcount, ws, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -323,20 +292,6 @@ cudaError_t launch_passBt_t(const Plan& p, const Dev& d, int kcount, const V* ws
   const unsigned grid = (unsigned)d.sms;
   return launch_counted(LK_PASSB, st, [&] {
     k_passBt<TP, CB, A2, V><<<grid, 256, pbt_smem(TP), st>>>(p.N, kcount, ws, al, partial);
-    return cudaGetLastError();
-  });
-}
-
-template <int CB, int L, bool A2>
-cudaError_t launch_passBr_t(const Dev& d, int kcount, const double* ws, const Alphas& al, double* partial,
-                            cudaStream_t st) {
-  static uint64_t init_mask = 0;   // per device: the attribute belongs to the device context
-  {
-    cudaError_t e = set_smem_once(k_passBr<CB, L, A2>, PBR_SMEM, init_mask);
-    if (e != cudaSuccess) return e;
-  }
-  return launch_counted(LK_PASSB, st, [&] {
-    k_passBr<CB, L, A2><<<d.sms, 256, PBR_SMEM, st>>>(kcount, ws, al, partial);
     return cudaGetLastError();
   });
 }
@@ -384,7 +339,7 @@ template <class V, bool A2>
 cudaError_t launch_passBp(const Plan& p, const Dev& d, int kcount, const V* ws, const Alphas& al, double* partial,
                           cudaStream_t st) {
   if constexpr (std::is_same<V, double>::value) {   // FP64 N = 21..24: radix-64 pass B (one transpose)
-    if (p.N >= 21 && p.N <= 24 && p.rowmajor) {
+    if (p.N >= 21 && p.N <= 24) {
       switch (13 - p.H) {
         case 5: return launch_passBw_t<5, 12, A2>(p, d, kcount, ws, al, partial, st);
         case 4: return launch_passBw_t<4, 12, A2>(p, d, kcount, ws, al, partial, st);
@@ -392,28 +347,12 @@ cudaError_t launch_passBp(const Plan& p, const Dev& d, int kcount, const V* ws, 
         case 2: return launch_passBw_t<2, 12, A2>(p, d, kcount, ws, al, partial, st);
       }
     }
-    if (p.N >= 21 && p.N <= 24 && !p.legacyB) {
-      switch (13 - p.H) {
-        case 5: return launch_passBr_t<5, 12, A2>(d, kcount, ws, al, partial, st);
-        case 4: return launch_passBr_t<4, 12, A2>(d, kcount, ws, al, partial, st);
-        case 3: return launch_passBr_t<3, 12, A2>(d, kcount, ws, al, partial, st);
-        case 2: return launch_passBr_t<2, 12, A2>(d, kcount, ws, al, partial, st);
-      }
-    }
-    if (p.N >= 17 && p.N <= 20 && p.rowmajor) {   // k_passA10s<ROWM> wrote row-major planes
-      switch (13 - p.H) {
+    if (p.N >= 17 && p.N <= 20) {
+      switch (13 - p.H) {   // FP64 N = 17..20: k_passA10s<ROWM> wrote row-major planes
         case 7: return launch_passBw_t<7, 10, A2>(p, d, kcount, ws, al, partial, st);
         case 6: return launch_passBw_t<6, 10, A2>(p, d, kcount, ws, al, partial, st);
         case 5: return launch_passBw_t<5, 10, A2>(p, d, kcount, ws, al, partial, st);
         case 4: return launch_passBw_t<4, 10, A2>(p, d, kcount, ws, al, partial, st);
-      }
-    }
-    if (p.N >= 17 && p.N <= 20) {   // k_passA10s wrote 2^13-double tiles for these (its cb = 13 - H)
-      switch (13 - p.H) {
-        case 7: return launch_passBr_t<7, 10, A2>(d, kcount, ws, al, partial, st);
-        case 6: return launch_passBr_t<6, 10, A2>(d, kcount, ws, al, partial, st);
-        case 5: return launch_passBr_t<5, 10, A2>(d, kcount, ws, al, partial, st);
-        case 4: return launch_passBr_t<4, 10, A2>(d, kcount, ws, al, partial, st);
       }
     }
   }

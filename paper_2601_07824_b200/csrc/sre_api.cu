@@ -164,17 +164,9 @@ int make_plan(int N, const Dev& d, Plan& p, uint64_t count = ~0ull) {
       p.staged = true;
       p.amin = 1ull << p.L;
       if (p.slots < 4 * 160) p.slots = 4 * 160;
-      const char* la = getenv("SRE_LEGACY_A");
-      p.legacyA = la && la[0] == '1';
-      const char* lb = getenv("SRE_LEGACY_B");
-      p.legacyB = lb && lb[0] == '1';
-      const char* sl = getenv("SRE_SLAB");
-      p.rowmajor = N <= 24 && !(sl && sl[0] == '1') && !p.legacyA && !p.legacyB;
     }
     if (p.L == 10) {  // staged pass A + persistent pass B (N = 15..20)
       p.staged = true;
-      const char* sl = getenv("SRE_SLAB");
-      p.rowmajor = N >= 17 && !(sl && sl[0] == '1');   // FP64 only: the FP32 kernels keep their slab layout
       p.KG = staged_groups(N);
       if ((uint64_t)8 * p.KG > count) p.KG = (int)((count + 7) / 8 > 0 ? (count + 7) / 8 : 1);
       if ((size_t)8 * p.KG > (size_t)p.K) {

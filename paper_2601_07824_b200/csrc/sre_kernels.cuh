@@ -808,6 +808,11 @@ __device__ __forceinline__ uint32_t pa10_freq(uint32_t pos) {
          (((t >> 4) & 1u) << 5) | ((r & 1u) << 6) | (((r >> 1) & 1u) << 9) | (((r >> 2) & 1u) << 4) |
          (((r >> 3) & 1u) << 2) | ((r >> 4) & 1u);
 }
+// k_passA10s<ROWM> stores (lane t, register r) at position 2 t + (r & 1) + 64 (r >> 1)
+__device__ __forceinline__ uint32_t pa10_freq_rowm(uint32_t pos) {
+  const uint32_t t = (pos >> 1) & 31u, r = (pos & 1u) | ((pos >> 6) << 1);
+  return pa10_freq(t + 32u * r);
+}
 __device__ __forceinline__ void tmem_st32d(uint32_t ta, const double (&v)[32]) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x64.b32 [%64], {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32, %33, %34, %35, %36, %37, %38, %39, %40, %41, %42, %43, %44, %45, %46, %47, %48, %49, %50, %51, %52, %53, %54, %55, %56, %57, %58, %59, %60, %61, %62, %63};\n"
                ::"r"(__double2loint(v[0])), "r"(__double2hiint(v[0])), "r"(__double2loint(v[1])), "r"(__double2hiint(v[1])), "r"(__double2loint(v[2])), "r"(__double2hiint(v[2])), "r"(__double2loint(v[3])), "r"(__double2hiint(v[3])),
@@ -866,9 +871,9 @@ template <int N, class V = double, bool ROWM = false>   // ROWM: row-major plane
 __global__ void __launch_bounds__(256, 1) k_passA10s(const typename Cx<V>::T* __restrict__ psi, uint64_t a_first,
                                                      int kcount, int groups, V* __restrict__ ws) {
   using C2 = typename Cx<V>::T;
-  // pass-B tile: 2^13 values for the FP64 radix-64 k_passBr (N = 17..20: 128-B or longer row runs),
-  // 2^12 for k_passBt (N = 15, 16 and the FP32 mode)
-  constexpr int cb = (std::is_same<V, double>::value && N >= 17 ? 13 : 12) - (N - 11);
+  // slab-major pass-B tiles of 2^12 values for k_passBt (N = 15, 16 and the FP32 mode); FP64 N >= 17
+  // writes row-major planes (ROWM) for the TMA-gather k_passBw
+  constexpr int cb = 12 - (N - 11);
   extern __shared__ __align__(128) double smem[];
   C2* ring = reinterpret_cast<C2*>(smem);                       // [NS][q row | r row][1024]
   V* exch = reinterpret_cast<V*>(smem + PA10_NS * 2 * 1024 * 2);   // [warp][padded 1024]
@@ -938,12 +943,13 @@ __global__ void __launch_bounds__(256, 1) k_passA10s(const typename Cx<V>::T* __
     if (active) {
       if constexpr (TM) transform10_tmem(tm, v);              // position lane + 32 j <- pa10_freq
       else Rounds<10, 0, 0, 2, BarWarp, true, V>::run(v, xw, lane, BarWarp{});
-      if constexpr (ROWM) {                                     // row-major: 8 KB per row, 256 B per store
-        V* w0 = ws + (size_t)k * 2 * plane + (yh << 10) + lane;
+      if constexpr (ROWM) {   // row-major: 8 KB per row; registers (2 i, 2 i + 1) of lane l go to positions
+        // 64 i + 2 l + {0, 1} as one 16-B store (512 contiguous bytes per warp instruction)
+        V* w0 = ws + (size_t)k * 2 * plane + (yh << 10) + 2 * lane;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          __stcg(w0 + 32 * j, v[0][j]);
-          __stcg(w0 + plane + 32 * j, v[1][j]);
+        for (int i = 0; i < 16; ++i) {
+          __stcg(reinterpret_cast<double2*>(w0 + 64 * i), make_double2(v[0][2 * i], v[0][2 * i + 1]));
+          __stcg(reinterpret_cast<double2*>(w0 + plane + 64 * i), make_double2(v[1][2 * i], v[1][2 * i + 1]));
         }
         continue;
       }
@@ -1176,269 +1182,13 @@ __device__ __forceinline__ void bfly64(double (&v)[64]) {
     }
 }
 
-// ------------------------------------------------------------------------------------------
-// Radix-64 streamed pass A for L = 12 (N = 21..24), FP64: k_passAq.
-// A 4096-point plane row is held by a unit of 64 threads x 64 values, so the 12 low bits take two
-// register rounds and ONE shared-memory transpose (k_passAs: 32 values per thread, three rounds).
-//   CTA = 4 units (256 threads); an item is (block of 4 consecutive rows 4m..4m+3, X-string k);
-//   unit u transforms row 4m + u.  Each unit streams its two psi rows (x_h = ins0(y_h, p - 12) and
-//   x_h ^ a_h) in 16 chunks of 256 complex (q chunk c, r chunk c ^ (a_l >> 8): 8 KB per stage)
-//   through its own 3-deep bulk-copy ring.  Generation computes both planes; plane A stays in
-//   registers, plane B is parked in TMEM (128 columns per thread) until plane A is stored.
-//   Round 0: register index j = pos bits 6..11 (pos = t + 64 j).  Transpose through the unit's
-//   32 KB XOR-swizzled buffer (physical = e ^ ((e >> 6) & 15): conflict-free both ways, no pad).
-//   Round 1: j = pos bits 0..5 (pos = 64 t + j); each thread writes 16 runs of 4 doubles into the
-//   slab-major workspace of k_passBr<CB = 13 - H> with 32-byte stores.
-// Why 4 rows of one X-string per CTA: at N = 24 a row's output is 32 B per pass-B slab, and HBM
-// absorbs such scattered 32-B runs at 1.9-2.2 TB/s when the four rows of each 128-B line come from
-// different CTAs at different times (k_passAr-style items, four X-strings of one row), but at
-// 3.3-3.7 TB/s when the four units of one CTA write them together (tools/microbench_wr.cu,
-// profiles/r02_microbench_write_patterns.txt).  CTA-staged whole-line stores (4.5 TB/s alone) and
-// 2-CTA clusters sharing psi rows over DSMEM measured slower here: their CTA/cluster barriers cost
-// more than the write pattern saves.
-// Items run X-string-fastest, so the K X-strings of a launch read each psi row pair from L2 after
-// its first HBM fetch.
-// ------------------------------------------------------------------------------------------
-constexpr int PAQ_NS = 3;                                             // ring stages per unit
-constexpr int PAQ_CH = 256;                                           // complex per chunk
-constexpr int PAQ_SMEM = 4 * PAQ_NS * 2 * PAQ_CH * 16 + 4 * 4096 * 8;  // 96 KB rings + 128 KB transposes
-__device__ __forceinline__ uint32_t xsw12(uint32_t e) { return e ^ ((e >> 6) & 15u); }
-__device__ __forceinline__ void tmem_st4d(uint32_t ta, const double (&v)[4]) {         // 4 doubles -> 8 columns
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%8], {%0, %1, %2, %3, %4, %5, %6, %7};\n"
-               ::"r"(__double2loint(v[0])), "r"(__double2hiint(v[0])), "r"(__double2loint(v[1])), "r"(__double2hiint(v[1])),
-                 "r"(__double2loint(v[2])), "r"(__double2hiint(v[2])), "r"(__double2loint(v[3])), "r"(__double2hiint(v[3])),
-                 "r"(ta) : "memory");
-}
+__device__ __forceinline__ uint32_t xsw12(uint32_t e) { return e ^ ((e >> 6) & 15u); }   // radix-64 transpose swizzle
 
-template <int N>
-__global__ void __launch_bounds__(256, 1) k_passAq(const double2* __restrict__ psi, uint64_t a_first, int kcount,
-                                                   uint64_t kmagic, double* __restrict__ ws) {
-  constexpr int L = 12, H = N - 1 - L, CB = 13 - H;
-  static_assert(H >= 8 && H <= 11, "k_passAq covers N = 21..24");
-  constexpr uint64_t RBLK = 1ull << (H - 2);                          // 4-row blocks per plane
-  constexpr size_t PLANE = (size_t)1 << (N - 1);
-  extern __shared__ __align__(128) double smem[];
-  double2* rings = reinterpret_cast<double2*>(smem);                 // [unit][NS][q 256 | r 256]
-  double* exch = smem + 4 * PAQ_NS * 2 * PAQ_CH * 2;                  // [unit][4096]
-  __shared__ __align__(8) uint64_t full[4][PAQ_NS];
-  __shared__ int used[4][PAQ_NS];
-  __shared__ uint32_t tmem_s;
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int u = w >> 1;
-  const uint32_t t = threadIdx.x & 63;
-  const uint64_t items = RBLK * (uint64_t)kcount;
-  const uint64_t my_items = items > blockIdx.x ? (items - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const uint64_t stages = my_items * 16;
-  // item -> (m, k) = (item / kcount, item % kcount) without a division: kmagic = ceil(2^40 / kcount),
-  // exact for item < 2^40 / kcount^2 (items <= 2^9 x 512 here)
-  auto split = [&](uint64_t item, uint64_t& m, uint64_t& k) {
-    m = (item * kmagic) >> 40;
-    k = item - m * (uint64_t)kcount;
-  };
-  if (w == 0) tmem_alloc(&tmem_s, 256);
-  if (threadIdx.x == 32) {
-    for (int x = 0; x < 4; ++x)
-      for (int i = 0; i < PAQ_NS; ++i) { mbar_init(&full[x][i], 1); used[x][i] = 0; }
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  tmem_fence_before();
-  __syncthreads();
-  tmem_fence_after();
-  const uint32_t tm = tmem_s + ((uint32_t)(32 * (w & 3)) << 16) + 128u * (uint32_t)(w >> 2);
-  double2* ring = rings + (size_t)u * PAQ_NS * 2 * PAQ_CH;
-  auto produce = [&](uint64_t s, int slot) {                        // one thread of unit u
-    uint64_t m, kk;
-    split(blockIdx.x + (s >> 4) * gridDim.x, m, kk);
-    const uint32_t c = (uint32_t)(s & 15);
-    const uint64_t a = a_first + kk;
-    const int p = 63 - __clzll((long long)a);                        // >= 12
-    const uint64_t xh = ins0(4 * m + u, p - L);
-    const uint32_t ahi = (uint32_t)((a >> 8) & 15u);
-    double2* dst = ring + (size_t)slot * 2 * PAQ_CH;
-    mbar_expect_tx(&full[u][slot], 2 * PAQ_CH * sizeof(double2));
-    bulk_g2s(dst, psi + (xh << L) + PAQ_CH * c, PAQ_CH * sizeof(double2), &full[u][slot]);
-    bulk_g2s(dst + PAQ_CH, psi + ((xh ^ (a >> L)) << L) + PAQ_CH * (c ^ ahi), PAQ_CH * sizeof(double2), &full[u][slot]);
-  };
-  if (t == 0)
-    for (int i = 0; i < PAQ_NS; ++i)
-      if ((uint64_t)i < stages) produce(i, i);
-  double* xb = exch + (size_t)u * 4096;
-  const BarNamed bar{1 + u, 64};
-  uint64_t s = 0;
-  for (uint64_t li = 0; li < my_items; ++li) {
-    uint64_t m, k;
-    split(blockIdx.x + li * gridDim.x, m, k);
-    const uint32_t al = (uint32_t)((a_first + k) & 4095u);
-    const uint32_t alo = al & 63u, ajq = (al >> 6) & 3u;
-    double v[64];
-#pragma unroll
-    for (int c = 0; c < 16; ++c, ++s) {
-      const int slot = (int)(s % PAQ_NS);
-      mbar_wait(&full[u][slot], (uint32_t)(s / PAQ_NS) & 1u);
-      const double2* cq = ring + (size_t)slot * 2 * PAQ_CH;
-      double b4[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const double2 q = cq[t + 64 * i];
-        const double2 r = cq[PAQ_CH + (t ^ alo) + 64 * (i ^ ajq)];
-        v[4 * c + i] = fma(r.x, q.x, r.y * q.y);        // Re conj(psi_{x^a}) psi_x
-        b4[i] = fma(r.x, q.y, -(r.y * q.x));            // Im
-      }
-      tmem_st4d(tm + 8u * c, b4);
-      __syncwarp();
-      if (lane == 0) {                                   // release the stage; the unit's 2nd warp refills it
-        if (atomicAdd(&used[u][slot], 1) == 1) {
-          atomicExch(&used[u][slot], 0);
-          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-          if (s + PAQ_NS < stages) produce(s + PAQ_NS, slot);
-        }
-      }
-    }
-    tmem_wait_st();
-    double* wr = ws + (size_t)k * 2 * PLANE + ((4 * m + u) << CB);    // row 4m + u of slab 0
-    auto transform_store = [&](double* wp) {
-      bfly64(v);                                         // round 0: pos bits 6..11
-      bar.sync();                                        // previous readers of xb are done
-#pragma unroll
-      for (int j = 0; j < 64; ++j) xb[xsw12(t + 64u * j)] = v[j];
-      bar.sync();
-#pragma unroll
-      for (int j = 0; j < 64; ++j) v[j] = xb[xsw12(64u * t + j)];
-      bfly64(v);                                         // round 1: pos bits 0..5
-#pragma unroll
-      for (int r4 = 0; r4 < 16; ++r4) {
-        const uint32_t pos = 64u * t + 4u * r4;
-        const size_t off = ((size_t)(pos >> CB) << (H + CB)) + (pos & ((1u << CB) - 1u));
-        stg_v4(wp + off, v[4 * r4], v[4 * r4 + 1], v[4 * r4 + 2], v[4 * r4 + 3]);
-      }
-    };
-    transform_store(wr);                                 // plane A
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {                        // plane B back from TMEM
-      uint32_t r32[16];
-      tmem_ld8d(tm + 16u * c, r32);
-      tmem_wait_ld();
-#pragma unroll
-      for (int i = 0; i < 8; ++i) v[8 * c + i] = __hiloint2double(r32[2 * i + 1], r32[2 * i]);
-    }
-    transform_store(wr + PLANE);                         // plane B
-  }
-  tmem_fence_before();
-  __syncthreads();
-  if (w == 0) tmem_dealloc(tmem_s, 256);
-}
-
-// ------------------------------------------------------------------------------------------
-// Radix-64 pass B over 2^13-double tiles (FP64, N = 17..24): k_passBr<CB, L>.  A tile is the
-// contiguous slab of 2^H rows x 2^CB columns (H + CB = 13, element e = row * 2^CB + col) that
-// k_passA10s (L = 10) or k_passAq (L = 12) wrote; a unit of 128 threads holds it as 64 values per thread, so the H row bits take
-// two register rounds and ONE transpose (k_passBt<13, CB>: 32 values, three rounds).
-//   Round 0: registers = e bits 7..12 (the 6 high row bits), thread = e bits 0..6 (pos = t + 128 j).
-//   Round 1: registers = e bits 1..6 (the remaining H - 6 row bits and CB - 1 column bits),
-//            thread = e bit 0 and e bits 7..12; the power sums accumulate from here.
-//   The transpose runs in place in the tile's ring slot with physical index
-//   e ^ (((e >> 7) & 7) << 1): both layouts are conflict-free (half-warps hit 16 distinct banks).
-// A CTA runs two units over three 64 KB slots: CTA tile n sits in slot n % 3 and belongs to unit
-// n % 2; a unit hands its slot back (refill with tile n + 3) right after its round-1 loads.
-// ------------------------------------------------------------------------------------------
+// Radix-64 pass B transpose (k_passBw): tile element e = row * 2^CB + col, 2^13 per tile; round-0
+// registers e bits 7..12, round-1 registers e bits 1..6; physical e ^ (((e >> 7) & 7) << 1) is
+// conflict-free for both layouts (tests/test_layouts.py)
 constexpr int PBR_SMEM = 3 * 8192 * 8;
 __device__ __forceinline__ uint32_t xsw13(uint32_t e) { return e ^ (((e >> 7) & 7u) << 1); }
-
-template <int CB, int L, bool A2>
-__global__ void __launch_bounds__(256, 1) k_passBr(int kcount, const double* __restrict__ ws, Alphas al,
-                                                   double* partial) {
-  ln_table_init(!A2 && al.need_log && std::is_same<double, double>::value);   // t ln t pass (tile_accumulate)
-  constexpr int H = 13 - CB;
-  static_assert(H >= 6 && H <= 11, "k_passBr: 6 to 11 row bits (N = 17..20 with L = 10, N = 21..24 with L = 12)");
-  extern __shared__ __align__(128) double smem[];
-  __shared__ __align__(8) uint64_t full[3];
-  __shared__ volatile unsigned long long issued[3];
-  __shared__ unsigned long long shist[SPEC_BINS];
-  const int u = threadIdx.x >> 7;
-  const uint32_t t = threadIdx.x & 127;
-  const uint64_t slabs = 1ull << (L - CB);
-  const uint64_t tiles = (uint64_t)kcount * 2 * slabs;
-  const uint64_t my_tiles = tiles > blockIdx.x ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const BarNamed bar{1 + u, 128};
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < 3; ++i) { mbar_init(&full[i], 1); issued[i] = ~0ull; }
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  if (al.hist)
-    for (int i = threadIdx.x; i < SPEC_BINS; i += blockDim.x) shist[i] = 0ull;
-  __syncthreads();
-  // issued[slot] = the CTA tile whose copy targets the slot.  A unit may only wait on a slot's
-  // mbarrier once its own tile has been issued there: tile n - 3 (the previous occupant) belongs to
-  // the other unit, so without this check a fast unit could test the parity of a phase two
-  // completions ahead, read early, and have a second copy land in the same slot.
-  auto issue = [&](uint64_t n) {                                   // one thread
-    const int slot = (int)(n % 3);
-    issued[slot] = n;
-    mbar_expect_tx(&full[slot], 8192 * sizeof(double));
-    bulk_g2s(smem + (size_t)slot * 8192, ws + (blockIdx.x + n * gridDim.x) * 8192, 8192 * sizeof(double), &full[slot]);
-  };
-  if (threadIdx.x == 0)
-    for (uint64_t n = 0; n < 3 && n < my_tiles; ++n) issue(n);
-  double acc[NACC];
-#pragma unroll
-  for (int i = 0; i < NACC; ++i) acc[i] = 0.0;
-  for (uint64_t n = (uint64_t)u; n < my_tiles; n += 2) {
-    const int slot = (int)(n % 3);
-    double* buf = smem + (size_t)slot * 8192;
-    while (issued[slot] != n) __nanosleep(32);
-    mbar_wait(&full[slot], (uint32_t)(n / 3) & 1u);
-    double v[64];
-#pragma unroll
-    for (int j = 0; j < 64; ++j) v[j] = buf[t + 128u * j];      // round-0 layout, natural order
-    bfly64(v);                                                   // 6 high row bits
-    bar.sync();                                                  // every thread has read the tile
-#pragma unroll
-    for (int j = 0; j < 64; ++j) buf[xsw13(t + 128u * j)] = v[j];
-    bar.sync();
-    const uint32_t tb = (t & 1u) | ((t >> 1) << 7);
-#pragma unroll
-    for (int j = 0; j < 64; ++j) v[j] = buf[xsw13(tb | ((uint32_t)j << 1))];
-    bar.sync();                                                  // slot free
-    if (t == 0) {
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      if (n + 3 < my_tiles) issue(n + 3);
-    }
-    // round 1: register bits 0..5 = e bits 1..6; the low (H - 6) of them... all 6 are butterflied
-    // except the column bits (e bits < CB), which index independent columns
-    constexpr int CLO = CB - 1;                                  // column bits among register bits 0..5
-#pragma unroll
-    for (int h = 1 << CLO; h < 64; h <<= 1)
-#pragma unroll
-      for (int i = 0; i < 64; ++i) {
-        if (i & h) continue;
-        const double a = v[i], b = v[i + h];
-        v[i] = a + b;
-        v[i + h] = a - b;
-      }
-    tile_accumulate<A2>(acc, v, al);
-    if (al.hist) spec_add(shist, v);
-    if (al.chi) {     // sre_chi: register j holds tile element e = (t & 1) | (j << 1) | ((t >> 1) << 7)
-      const uint64_t tile = blockIdx.x + n * gridDim.x;
-      const uint64_t kp = tile / slabs, slab = tile % slabs;
-      const uint64_t a = al.chi_a0 + (kp >> 1);
-      const int p = pivot_of(a, L + H + 1);
-#pragma unroll
-      for (int j = 0; j < 64; ++j) {
-        const uint32_t e = tb | ((uint32_t)j << 1);
-        const uint64_t pos = (slab << CB) | (e & ((1u << CB) - 1u));
-        // k_passAq: position = frequency; k_passA10s: frequency pa10_freq(pos) sits at pos = lane + 32 j
-        const uint64_t bl = L == 10 ? pa10_freq((uint32_t)pos) : pos;
-        chi_store(al.chi, a, p, (int)(kp & 1), ((uint64_t)(e >> CB) << L) | bl, v[j]);
-      }
-    }
-  }
-  block_flush(acc, partial, blockIdx.x);
-  if (al.hist) {
-    __syncthreads();
-    for (int i = threadIdx.x; i < SPEC_BINS; i += blockDim.x)
-      if (shist[i]) atomicAdd(al.hist + i, shist[i]);
-  }
-}
 
 // ------------------------------------------------------------------------------------------
 // Row-major streamed path for N = 21..24 (FP64): k_passAw + k_passBw.
@@ -1446,12 +1196,14 @@ __global__ void __launch_bounds__(256, 1) k_passBr(int kcount, const double* __r
 // 32 KB row contiguously (coalesced 16-B stores: HBM takes contiguous writes at ~6.3 TB/s against
 // 3.3-3.7 TB/s for the 32-B runs a slab-major layout forces, tools/microbench_wr.cu), and pass B
 // gathers a tile of 2^H rows x 2^CB columns with TMA tensor copies (32-B pieces at a 32 KB stride
-// read at 5.2 TB/s vs 7.3 for contiguous tiles) into the same smem layout k_passBr uses.
+// read at 5.2 TB/s vs 7.3 for contiguous tiles) into the smem layout of the radix-64 transform.
 // ------------------------------------------------------------------------------------------
 // k_passAw: CTA = 4 units x 64 threads; an item is (row y_h, group of 4 consecutive X-strings);
 // unit u takes X-string 4g + u.  The 4 X-strings share a_h and a_l >> 9, hence both psi rows and
 // every chunk: one ring of 16 KB stages (q chunk c, r chunk c ^ (a_l >> 9), 512 complex each) is
-// read by all 8 warps.  Radix-64 rounds as k_passAq; plane B parked in TMEM.  After round 1 the
+// read by all 8 warps.  Radix-64: a 4096-point row-plane is 64 threads x 64 values, two register
+// rounds around ONE XOR-swizzled transpose (round 0: pos = t + 64 j, bits 6..11 in registers; round 1:
+// pos = 64 t + j); plane B parked in TMEM (128 columns per thread).  After round 1 the
 // unit stages its row in natural position order in its XOR-swizzled buffer and stores it with
 // coalesced 16-B stores.
 constexpr int PAW_NS = 4;                                             // ring stages (16 KB each)
@@ -1591,7 +1343,7 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tmap, 
                : "memory");
 }
 
-// k_passBw: k_passBr's transform over the row-major planes of k_passAw (L = 12) or k_passA10s<ROWM>
+// k_passBw: radix-64 pass B over the row-major planes of k_passAw (L = 12) or k_passA10s<ROWM>
 // (L = 10).  Tile (plane kp = 2k + p, column group s) = 2^H rows x 2^CB columns, gathered by 2^H / R
 // TMA boxes of R = min(256, 2^H) rows x 2^CB columns (tensor map: dims {2^L, 2^H, 2K}) into the slot
 // as e = row * 2^CB + col.
@@ -1619,7 +1371,10 @@ __global__ void __launch_bounds__(256, 1) k_passBw(int kcount, const __grid_cons
   if (al.hist)
     for (int i = threadIdx.x; i < SPEC_BINS; i += blockDim.x) shist[i] = 0ull;
   __syncthreads();
-  // issued[slot]: as in k_passBr (the two units share the three slots)
+  // issued[slot] = the CTA tile whose copy targets the slot.  The two units share three slots, so a
+  // unit may only wait on a slot's mbarrier once its own tile has been issued there (tile n - 3, the
+  // previous occupant, belongs to the other unit: testing the parity early could read a phase two
+  // completions ahead and let a second copy land in the slot).
   auto issue = [&](uint64_t n) {                                   // one thread
     const int slot = (int)(n % 3);
     issued[slot] = n;
@@ -1677,7 +1432,7 @@ __global__ void __launch_bounds__(256, 1) k_passBw(int kcount, const __grid_cons
       for (int j = 0; j < 64; ++j) {
         const uint32_t e = tb | ((uint32_t)j << 1);
         const uint64_t pos = (slab << CB) | (e & ((1u << CB) - 1u));
-        const uint64_t bl = L == 10 ? pa10_freq((uint32_t)pos) : pos;   // k_passA10s: TMEM-transposed order
+        const uint64_t bl = L == 10 ? pa10_freq_rowm((uint32_t)pos) : pos;   // k_passA10s<ROWM> store order
         chi_store(al.chi, a, p, (int)(kp & 1), ((uint64_t)(e >> CB) << L) | bl, v[j]);
       }
     }

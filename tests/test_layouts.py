@@ -86,3 +86,16 @@ def test_row_staging_reads_pairs():
         assert (xsw12(e), xsw12(e + 1)) == got
     for q in range(0, 2048, 8):
         assert len({((2 * c) ^ ((2 * c >> 6) & 15)) // 2 % 8 for c in range(q, q + 8)}) == 8
+
+
+def test_rowmajor_store_order_is_a_permutation():
+    """k_passA10s<ROWM> writes (lane t, register r) at position 2 t + (r & 1) + 64 (r >> 1); the chi
+    decode (pa10_freq_rowm) inverts it."""
+    seen = set()
+    for t in range(32):
+        for r in range(32):
+            pos = 2 * t + (r & 1) + 64 * (r >> 1)
+            tt, rr = (pos >> 1) & 31, (pos & 1) | ((pos >> 6) << 1)
+            assert (tt, rr) == (t, r)
+            seen.add(pos)
+    assert seen == set(range(1024))
