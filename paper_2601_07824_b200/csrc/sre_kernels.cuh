@@ -834,27 +834,41 @@ __device__ __forceinline__ void tmem_ld16x256(uint32_t ta, double* v) {     // 1
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __hiloint2double(u[2 * i + 1], u[2 * i]);
 }
-// one trip of both planes: plane p at double columns [32 p, 32 p + 32) of this warp's TMEM slice
-__device__ __forceinline__ void tmem_trip2(uint32_t tm, double (&v)[2][32]) {
-  tmem_st32d(tm, v[0]);
-  tmem_st32d(tm + 64u, v[1]);
-  tmem_wait_st();
-  tmem_ld16x256(tm, v[0]);
-  tmem_ld16x256(tm + (16u << 16), v[0] + 16);
-  tmem_ld16x256(tm + 64u, v[1]);
-  tmem_ld16x256(tm + 64u + (16u << 16), v[1] + 16);
-  tmem_wait_ld();
-}
 template <int B>
 __device__ __forceinline__ void bfly_bit(double (&v)[32]) { bfly32<B, B + 1>(v); }
+__device__ __forceinline__ void tmem_ld_plane(uint32_t ta, double (&v)[32]) {
+  tmem_ld16x256(ta, v);
+  tmem_ld16x256(ta + (16u << 16), v + 16);
+}
+// The two planes' trips are interleaved so that one plane's butterflies run while the other plane's
+// tcgen05.st/ld are in flight (the waits cover every outstanding op of the thread):
+//   st A1 st B1 | wait.st | ld A1 ld B1 | wait.ld | bfly A, st A2 | bfly B, st B2 | wait.st | ...
 __device__ __forceinline__ void transform10_tmem(uint32_t tm, double (&v)[2][32]) {
-  bfly32<0, 5>(v[0]); bfly32<0, 5>(v[1]);                 // e bits 5..9
-  tmem_trip2(tm, v);
-  bfly_bit<0>(v[0]); bfly_bit<4>(v[0]); bfly_bit<0>(v[1]); bfly_bit<4>(v[1]);   // e3, e4
-  tmem_trip2(tm, v);
-  bfly_bit<0>(v[0]); bfly_bit<4>(v[0]); bfly_bit<0>(v[1]); bfly_bit<4>(v[1]);   // e1, e2
-  tmem_trip2(tm, v);
-  bfly_bit<4>(v[0]); bfly_bit<4>(v[1]);                                           // e0
+  bfly32<0, 5>(v[0]);                                     // e bits 5..9
+  tmem_st32d(tm, v[0]);
+  bfly32<0, 5>(v[1]);
+  tmem_st32d(tm + 64u, v[1]);
+  tmem_wait_st();
+  tmem_ld_plane(tm, v[0]);
+  tmem_ld_plane(tm + 64u, v[1]);
+  tmem_wait_ld();
+  bfly_bit<0>(v[0]); bfly_bit<4>(v[0]);                   // e3, e4
+  tmem_st32d(tm, v[0]);
+  bfly_bit<0>(v[1]); bfly_bit<4>(v[1]);
+  tmem_st32d(tm + 64u, v[1]);
+  tmem_wait_st();
+  tmem_ld_plane(tm, v[0]);
+  tmem_ld_plane(tm + 64u, v[1]);
+  tmem_wait_ld();
+  bfly_bit<0>(v[0]); bfly_bit<4>(v[0]);                   // e1, e2
+  tmem_st32d(tm, v[0]);
+  bfly_bit<0>(v[1]); bfly_bit<4>(v[1]);
+  tmem_st32d(tm + 64u, v[1]);
+  tmem_wait_st();
+  tmem_ld_plane(tm, v[0]);
+  tmem_ld_plane(tm + 64u, v[1]);
+  tmem_wait_ld();
+  bfly_bit<4>(v[0]); bfly_bit<4>(v[1]);                   // e0
 }
 
 constexpr int PA10_NS = 4;                                   // staging ring depth
