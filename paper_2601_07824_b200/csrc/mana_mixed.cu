@@ -33,6 +33,10 @@ int is_device_ptr(const void* ptr, bool& dev);
 }  // namespace sre_host
 
 namespace mixed {
+using sre::mbar_expect_tx;
+using sre::mbar_init;
+using sre::mbar_wait;
+using sre::smem_u32;
 
 __host__ __device__ constexpr long p3(int k) {
   long r = 1;
@@ -136,14 +140,15 @@ __device__ __forceinline__ void leg_stage(double2* tile, double2* g, long base, 
   }
 }
 
-template <int SP, int NL, int J, bool FINAL, int NT>
+// SMEM: the tile arrives in shared memory and (unless FINAL) leaves from it (k_legs_tma, TMA)
+template <int SP, int NL, int J, bool FINAL, int NT, bool SMEM = false>
 __device__ __forceinline__ void leg_stages(double2* tile, double2* g, long base, long sR, long sC, double& aa,
                                            double& as) {
   if constexpr (J < NL) {
-    constexpr bool first = (J == 0), last = (J == NL - 1);
-    leg_stage<SP, NL, J, first, last && !FINAL, last && FINAL, NT>(tile, g, base, sR, sC, aa, as);
+    constexpr bool first = (J == 0) && !SMEM, last = (J == NL - 1);
+    leg_stage<SP, NL, J, first, last && !FINAL && !SMEM, last && FINAL, NT>(tile, g, base, sR, sC, aa, as);
     __syncthreads();
-    leg_stages<SP, NL, J + 1, FINAL, NT>(tile, g, base, sR, sC, aa, as);
+    leg_stages<SP, NL, J + 1, FINAL, NT, SMEM>(tile, g, base, sR, sC, aa, as);
   }
 }
 
@@ -234,6 +239,150 @@ __global__ void __launch_bounds__(NT) k_legs(LegArgs A) {
     }
   }
   if constexpr (FINAL) flush(aa, as, A.slots);
+}
+
+// Tile passes with TMA tiles (k_legs_tma).  The pass (SP, NL, k0) tile is one tensor box of the
+// column-major rho viewed as a 5-D tensor (fastest first):
+//     d0 = (r digits [0, SP), re/im)  extent 2 3^SP doubles         box 2 3^SP
+//     d1 = r digits [SP, k0)           extent 3^(k0-SP)              box 1
+//     d2 = r digits [k0, N)            extent 3^(N-k0)               box 3^NL (the row legs)
+//     d3 = c digits [0, k0)            extent 3^k0                   box 1
+//     d4 = c digits [k0, N)            extent 3^(N-k0)               box 3^NL (the column legs)
+// whose shared-memory image is exactly tile[s + 3^SP (R + 3^NL C)] (R5); the first pass (k0 = 0,
+// SP = 0) is the 2-D view {2 3^N doubles, 3^N columns}, box {2 3^NL, 3^NL} (contiguous 81-element
+// runs).  Item it = rl + nrl (rh + nrh (cl + ncl ch)) as in k_legs.  Persistent CTAs double-buffer
+// the tiles: item n + 1's box lands while item n runs its legs in shared memory; a non-final pass
+// stores the tile with one TMA tensor store, and the buffer is reloaded once that store has read it.
+__host__ __device__ constexpr int tile_elems(int SP, int NL) { return (int)p3(SP) * (int)p3(2 * NL); }
+__host__ __device__ constexpr int tile_stride(int SP, int NL) { return (tile_elems(SP, NL) + 7) & ~7; }   // 128-B aligned
+
+template <bool R5>
+__device__ __forceinline__ void tma_tile_load(void* dst, const CUtensorMap* tm, const int (&c)[5], uint64_t* bar) {
+  if constexpr (R5)
+    asm volatile("cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n"
+                 ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(tm)), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]),
+                 "r"(c[4]), "r"(smem_u32(bar)) : "memory");
+  else
+    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n"
+                 ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(tm)), "r"(c[0]), "r"(c[1]), "r"(smem_u32(bar))
+                 : "memory");
+}
+template <bool R5>
+__device__ __forceinline__ void tma_tile_store(const CUtensorMap* tm, const int (&c)[5], const void* src) {
+  if constexpr (R5)
+    asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];\n"
+                 ::"l"(reinterpret_cast<uint64_t>(tm)), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]),
+                 "r"(smem_u32(src)) : "memory");
+  else
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n"
+                 ::"l"(reinterpret_cast<uint64_t>(tm)), "r"(c[0]), "r"(c[1]), "r"(smem_u32(src)) : "memory");
+  asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+}
+
+__device__ __forceinline__ constexpr int ord81(int J, int i) {
+  constexpr int o[4][6] = {{5, 6, 7, 2, 1, 3}, {4, 7, 6, 3, 0, 2}, {5, 4, 7, 0, 1, 3}, {4, 5, 6, 1, 0, 2}};
+  return o[J][i];
+}
+template <int J, int NT>
+__device__ __forceinline__ void leg81(double2* tile) {
+  constexpr int PJ = (int)p3(J), sr = PJ, sc = 81 * PJ;
+#pragma unroll 2
+  for (int f = threadIdx.x; f < 729; f += NT) {
+    int q = f, tb = 0;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+      const int d = q % 3, k = ord81(J, i);
+      q /= 3;
+      tb += d * (k < 4 ? (int)p3(k) : 81 * (int)p3(k - 4));
+    }
+    double2 x[3][3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) x[r][c] = tile[tb + r * sr + c * sc];
+    leg9(x);
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) tile[tb + a * sr + b * sc] = x[a][b];
+  }
+  __syncthreads();
+}
+
+template <int SP, int NL, bool FINAL, bool R5, int NT>
+__global__ void __launch_bounds__(NT) k_legs_tma(LegArgs A, const __grid_constant__ CUtensorMap tm) {
+  constexpr int E = tile_elems(SP, NL), TS = tile_stride(SP, NL), B3 = (int)p3(NL);
+  extern __shared__ __align__(128) double2 tbuf[];
+  __shared__ __align__(8) uint64_t full[2];
+  const int N = A.N, k0 = A.k0;
+  const long nrl = p3(k0 - SP), nrh = p3(N - k0 - NL), ncl = p3(k0);
+  const long items = A.items;
+  auto coords = [&](long it, int (&c)[5]) {
+    const long rl = it % nrl;
+    long x = it / nrl;
+    const long rh = x % nrh;
+    x /= nrh;
+    const long cl = x % ncl, ch = x / ncl;
+    if constexpr (R5) {
+      c[0] = 0;
+      c[1] = (int)rl;
+      c[2] = (int)(B3 * rh);
+      c[3] = (int)cl;
+      c[4] = (int)(B3 * ch);
+    } else {
+      c[0] = (int)(2 * B3 * rh);
+      c[1] = (int)(B3 * ch);
+      c[2] = c[3] = c[4] = 0;
+    }
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const long it = blockIdx.x + (long)b * gridDim.x;
+      if (it < items) {
+        int c[5];
+        coords(it, c);
+        mbar_expect_tx(&full[b], E * sizeof(double2));
+        tma_tile_load<R5>(tbuf + b * TS, &tm, c, &full[b]);
+      }
+    }
+  }
+  __syncthreads();
+  double aa = 0.0, as = 0.0;
+  int n = 0;
+  for (long it = blockIdx.x; it < items; it += gridDim.x, ++n) {
+    const int b = n & 1;
+    double2* tile = tbuf + b * TS;
+    mbar_wait(&full[b], (n >> 1) & 1);
+    if constexpr (SP == 0 && NL == 4 && !FINAL) {
+      leg81<0, NT>(tile);
+      leg81<1, NT>(tile);
+      leg81<2, NT>(tile);
+      leg81<3, NT>(tile);
+    } else {
+      leg_stages<SP, NL, 0, FINAL, NT, true>(tile, A.rho, 0, 0, 0, aa, as);
+    }                                      // both end with __syncthreads: every thread is done with tile
+    if (threadIdx.x == 0) {
+      int c[5];
+      if constexpr (!FINAL) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // generic writes -> TMA reads
+        coords(it, c);
+        tma_tile_store<R5>(&tm, c, tile);
+      }
+      const long nx = it + 2 * (long)gridDim.x;
+      if (nx < items) {
+        if constexpr (!FINAL) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");   // store read buffer b
+        coords(nx, c);
+        mbar_expect_tx(&full[b], E * sizeof(double2));
+        tma_tile_load<R5>(tile, &tm, c, &full[b]);
+      }
+    }
+  }
+  if constexpr (FINAL) flush(aa, as, A.slots);
+  else if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
 }
 
 __global__ void __launch_bounds__(256) k_mixed_reduce(const double* slots, int n, double* out) {
@@ -359,6 +508,78 @@ int occupancy(const void* fn, size_t smem, int threads) {
   return occ;
 }
 
+bool use_tma() {   // SRE_MIXED_TMA=0: the LDG/STG k_legs tile passes (A/B measurements)
+  const char* e = std::getenv("SRE_MIXED_TMA");
+  return !(e && std::atoi(e) == 0);
+}
+
+using TmaFn = void (*)(mixed::LegArgs, CUtensorMap);
+template <bool F>
+TmaFn tma_fn_t(int sp, int nl, bool r5) {
+  if (!r5) {   // first pass: the 2-D view
+    switch (sp * 10 + nl) {
+      case 2: return mixed::k_legs_tma<0, 2, F, false, kThreads>;
+      case 3: return mixed::k_legs_tma<0, 3, F, false, kThreads>;
+      case 4: return mixed::k_legs_tma<0, 4, F, false, kThreads>;
+    }
+    return nullptr;
+  }
+  switch (sp * 10 + nl) {
+    case 2: return mixed::k_legs_tma<0, 2, F, true, kThreads>;
+    case 3: return mixed::k_legs_tma<0, 3, F, true, kThreads>;
+    case 4: return mixed::k_legs_tma<0, 4, F, true, kThreads>;
+    case 22: return mixed::k_legs_tma<2, 2, F, true, kThreads>;
+    case 23: return mixed::k_legs_tma<2, 3, F, true, kThreads>;
+    case 32: return mixed::k_legs_tma<3, 2, F, true, kThreads>;
+    case 42: return mixed::k_legs_tma<4, 2, F, true, kThreads>;
+  }
+  return nullptr;
+}
+size_t tma_smem(int sp, int nl) { return 2 * (size_t)((mixed::p3(sp) * mixed::p3(2 * nl) + 7) & ~7L) * sizeof(double2); }
+
+// One tile pass with TMA tiles (k_legs_tma); returns -1 when no instance covers (SP, NL).
+int launch_legs_tma(const Pass& p, bool fin, double2* rho, int N, double* slots, const Dev& d, cudaStream_t st) {
+  const bool r5 = p.k0 > 0;
+  TmaFn f = fin ? tma_fn_t<true>(p.SP, p.NL, r5) : tma_fn_t<false>(p.SP, p.NL, r5);
+  if (!f) return -1;
+  auto enc = tensor_map_encoder();
+  if (!enc) return fail(SRE_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t D = (cuuint64_t)mixed::p3(N), S3 = (cuuint64_t)mixed::p3(p.SP), B3 = (cuuint64_t)mixed::p3(p.NL);
+  CUtensorMap tm;
+  CUresult cr;
+  const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  CUtensorMapL2promotion l2p = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;   // best of 0/64/128/256 on x10
+  if (const char* e = std::getenv("SRE_MIXED_L2P")) {   // experiments: 0, 64, 128, 256
+    const int v = std::atoi(e);
+    l2p = v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+        : v == 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_NONE;
+  }
+  if (r5) {
+    const cuuint64_t K0 = (cuuint64_t)mixed::p3(p.k0);
+    const cuuint64_t dims[5] = {2 * S3, K0 / S3, D / K0, K0, D / K0};
+    const cuuint64_t strides[4] = {S3 * 16, K0 * 16, D * 16, D * K0 * 16};   // bytes, dims 1..4
+    const cuuint32_t box[5] = {(cuuint32_t)(2 * S3), 1, (cuuint32_t)B3, 1, (cuuint32_t)B3};
+    cr = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, rho, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, l2p, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    const cuuint64_t dims[2] = {2 * D, D};
+    const cuuint64_t strides[1] = {D * 16};
+    const cuuint32_t box[2] = {(cuuint32_t)(2 * B3), (cuuint32_t)B3};
+    cr = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, rho, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, l2p, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  if (cr != CUDA_SUCCESS) return fail(SRE_ECUDA, "cuTensorMapEncodeTiled failed (N=%d SP=%d NL=%d k0=%d)", N, p.SP, p.NL, p.k0);
+  const size_t smem = tma_smem(p.SP, p.NL);
+  const long items = mixed::p3(2 * N) / (mixed::p3(p.SP) * mixed::p3(2 * p.NL));
+  long g = (long)occupancy((const void*)f, smem, kThreads) * d.sms;
+  if (g > items) g = items;
+  if (g > kSlots) g = kSlots;
+  const int grid = (int)g;
+  mixed::LegArgs A{rho, slots, N, p.k0, items};
+  XCK(launch_counted(fin ? LK_PASSB : LK_PASSA, st, [&] { f<<<grid, kThreads, smem, st>>>(A, tm); return cudaGetLastError(); }));
+  return SRE_OK;
+}
+
 int run_mixed(double2* rho, int N, char* ws, size_t ws_bytes, double* sums_dev, cudaStream_t st) {
   Dev d;
   int rc = get_dev(d);
@@ -370,6 +591,13 @@ int run_mixed(double2* rho, int N, char* ws, size_t ws_bytes, double* sums_dev, 
   for (size_t i = 0; i < passes.size(); ++i) {
     const Pass& p = passes[i];
     const bool fin = (i + 1 == passes.size());
+    if (p.NL > 1 && use_tma()) {
+      rc = launch_legs_tma(p, fin, rho, N, slots, d, st);
+      if (rc >= 0) {
+        if (rc) return rc;
+        continue;
+      }
+    }
     int threads = kThreads;
     if (p.SP == 0 && p.NL == 4) {
       const char* e = std::getenv("SRE_MIXED_T0");   // experiments: threads of the 81 x 81 pass
