@@ -99,3 +99,32 @@ def test_rowmajor_store_order_is_a_permutation():
             assert (tt, rr) == (t, r)
             seen.add(pos)
     assert seen == set(range(1024))
+
+
+def test_mixed_81_tile_fiber_orders():
+    """k_legs04 (mana_mixed.cu ord81): each leg's fiber order is a permutation of its six free tile
+    digits (so the 729 fibers cover the 81 x 81 tile once), and the bank-group model of
+    tools/mana_tile_order.py rates the four orders at 6768 wavefronts per tile (ideal 6624)."""
+    import os
+    import re
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = open(os.path.join(root, "paper_2601_07824_b200", "csrc", "mana_mixed.cu")).read()
+    body = re.search(r"constexpr int o\[4\]\[6\] = \{(.*?)\};", src).group(1)
+    orders = [[int(x) for x in grp.split(",")] for grp in re.findall(r"\{([^{}]*)\}", body)]
+    assert len(orders) == 4
+    for J, o in enumerate(orders):
+        assert sorted(o) == sorted([k for k in range(4) if k != J] + [4 + k for k in range(4) if k != J])
+        covered = set()
+        for f in range(729):
+            tb, q = 0, f
+            for k in o:
+                tb += (q % 3) * (3 ** k if k < 4 else 81 * 3 ** (k - 4))
+                q //= 3
+            for r in range(3):
+                for c in range(3):
+                    covered.add(tb + r * 3 ** J + 81 * c * 3 ** J)
+        assert covered == set(range(6561))
+    sys.path.insert(0, os.path.join(root, "tools"))
+    from mana_tile_order import leg_cost
+    assert sum(leg_cost(J, orders[J]) for J in range(4)) == 6768
