@@ -8,6 +8,7 @@
 #include <atomic>
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 #include <type_traits>
 #include <utility>
@@ -232,21 +233,48 @@ cudaError_t launch_passAs_t(const Dev& d, const typename Cx<V>::T* psi, uint64_t
   });
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda at link time)
+inline PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
 template <int N>
 cudaError_t launch_passAw_t(const Dev& d, const double2* psi, uint64_t a_first, int kcount, double* ws, cudaStream_t st) {
-  static const bool cs = [] { const char* e = getenv("SRE_PAW_CS"); return e && e[0] == '1'; }();
-  static uint64_t init_mask = 0, init_mask_cs = 0;
+  static const bool ts = [] { const char* e = getenv("SRE_PAW_TMA"); return !(e && e[0] == '0'); }();
+  static uint64_t init_mask = 0, init_mask_ts = 0;
   {
-    cudaError_t e = cs ? set_smem_once(k_passAw<N, true>, PAW_SMEM, init_mask_cs) : set_smem_once(k_passAw<N, false>, PAW_SMEM, init_mask);
+    cudaError_t e = ts ? set_smem_once(k_passAw<N, true>, PAW_SMEM, init_mask_ts) : set_smem_once(k_passAw<N, false>, PAW_SMEM, init_mask);
     if (e != cudaSuccess) return e;
+  }
+  // TMA store map: row-plane r = (2k + p) 2^H + y_h as the 64 x 64 matrix [t][j], boxes {16, 64, 1}
+  CUtensorMap tm;
+  std::memset(&tm, 0, sizeof(tm));
+  if (ts) {
+    auto enc = tensor_map_encoder();
+    if (!enc) return cudaErrorNotSupported;
+    const cuuint64_t dims[3] = {64, 64, (cuuint64_t)kcount << (N - 12)};
+    const cuuint64_t strides[2] = {64 * sizeof(double), 4096 * sizeof(double)};
+    const cuuint32_t box[3] = {16, 64, 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, ws, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
   }
   const uint64_t groups = (uint64_t)(kcount + 3) / 4;
   const uint64_t items = groups << (N - 13);                         // (row, group of 4 X-strings)
   const unsigned grid = (unsigned)(items < (uint64_t)d.sms ? items : (uint64_t)d.sms);
   const uint64_t gmagic = ((1ull << 40) + groups - 1) / groups;
   return launch_counted(LK_PASSA, st, [&] {
-    if (cs) k_passAw<N, true><<<grid, 256, PAW_SMEM, st>>>(psi, a_first, kcount, gmagic, ws);
-    else k_passAw<N, false><<<grid, 256, PAW_SMEM, st>>>(psi, a_first, kcount, gmagic, ws);
+    if (ts) k_passAw<N, true><<<grid, 256, PAW_SMEM, st>>>(psi, a_first, kcount, gmagic, ws, tm);
+    else k_passAw<N, false><<<grid, 256, PAW_SMEM, st>>>(psi, a_first, kcount, gmagic, ws, tm);
     return cudaGetLastError();
   });
 }
@@ -294,19 +322,6 @@ cudaError_t launch_passBt_t(const Plan& p, const Dev& d, int kcount, const V* ws
     k_passBt<TP, CB, A2, V><<<grid, 256, pbt_smem(TP), st>>>(p.N, kcount, ws, al, partial);
     return cudaGetLastError();
   });
-}
-
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda at link time)
-inline PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
-    void* f = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      f = nullptr;
-    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
-  }();
-  return fn;
 }
 
 template <int CB, int L, bool A2>

@@ -1218,19 +1218,30 @@ __device__ __forceinline__ uint32_t xsw13(uint32_t e) { return e ^ (((e >> 7) & 
 // read by all 8 warps.  Radix-64: a 4096-point row-plane is 64 threads x 64 values, two register
 // rounds around ONE XOR-swizzled transpose (round 0: pos = t + 64 j, bits 6..11 in registers; round 1:
 // pos = 64 t + j); plane B parked in TMEM (128 columns per thread).  After round 1 the
-// unit stages its row in natural position order in its XOR-swizzled buffer and stores it with
-// coalesced 16-B stores.
+// unit stores its row with TMA (TS): the row-plane is the 64 x 64 matrix [t][j] (pos = 64 t + j), four
+// tensor boxes of {16 doubles, 64 rows} with SWIZZLE_128B; thread t writes its pairs (v[j], v[j+1])
+// as 16-B chunks at row t, chunk ((j & 15) >> 1) ^ (t & 7) of box j >> 4 (conflict-free per
+// quarter-warp), and the TMA engine reads the 32 KB back from shared memory and writes whole 128-B
+// lines -- no LDS/STG wavefronts on the L1TEX pipe.  !TS: natural-order staging in the XOR-swizzled
+// buffer and coalesced 16-B stores (A/B measurements, SRE_PAW_TMA=0).
 constexpr int PAW_NS = 4;                                             // ring stages (16 KB each)
-constexpr int PAW_SMEM = PAW_NS * 2 * 512 * 16 + 4 * 4096 * 8;        // 64 KB ring + 4 x 32 KB buffers
+constexpr int PAW_SMEM = PAW_NS * 2 * 512 * 16 + 4 * 4096 * 8 + 1024; // 64 KB ring + 4 x 32 KB buffers + alignment
 
-template <int N, bool PAW_CS>
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* tmap, int c0, int c1, int c2, const void* src) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n"
+               ::"l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(src)) : "memory");
+}
+
+template <int N, bool TS>
 __global__ void __launch_bounds__(256, 1) k_passAw(const double2* __restrict__ psi, uint64_t a_first, int kcount,
-                                                   uint64_t gmagic, double* __restrict__ ws) {
+                                                   uint64_t gmagic, double* __restrict__ ws,
+                                                   const __grid_constant__ CUtensorMap tmw) {
   constexpr int L = 12, H = N - 1 - L;
   static_assert(H >= 8 && H <= 11, "k_passAw covers N = 21..24");
   constexpr uint64_t ROWS = 1ull << H;
   constexpr size_t PLANE = (size_t)1 << (N - 1);
-  extern __shared__ __align__(128) double smem[];
+  extern __shared__ __align__(128) double smem_raw[];
+  double* smem = smem_raw + (((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u) >> 3);   // SWIZZLE_128B: 1024-B aligned
   double2* ring = reinterpret_cast<double2*>(smem);                 // [NS][q 512 | r 512]
   double* exch = smem + PAW_NS * 2 * 512 * 2;                        // [unit][4096]
   __shared__ __align__(8) uint64_t full[PAW_NS];
@@ -1309,8 +1320,10 @@ __global__ void __launch_bounds__(256, 1) k_passAw(const double2* __restrict__ p
     if (!active) continue;
     tmem_wait_st();
     double* wrow = ws + ((size_t)k * 2 << (N - 1)) + (yh << L);
-    auto transform_store = [&](double* wp) {
+    auto transform_store = [&](double* wp, int p) {
       bfly64(v);                                         // round 0: pos bits 6..11
+      if constexpr (TS)
+        if (t == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");   // last TMA store read xb
       bar.sync();                                        // previous readers of xb are done
 #pragma unroll
       for (int j = 0; j < 64; ++j) xb[xsw12(t + 64u * j)] = v[j];
@@ -1319,22 +1332,37 @@ __global__ void __launch_bounds__(256, 1) k_passAw(const double2* __restrict__ p
       for (int j = 0; j < 64; ++j) v[j] = xb[xsw12(64u * t + j)];
       bar.sync();                                        // the transpose reads are done: reuse xb
       bfly64(v);                                         // round 1: pos bits 0..5 (pos = 64 t + j)
+      if constexpr (TS) {
 #pragma unroll
-      for (int j = 0; j < 64; ++j) xb[xsw12(64u * t + j)] = v[j];
-      bar.sync();
-      // chunk C = t + 64 i holds positions 2C, 2C + 1: one 16-B load (halves swapped when the XOR key
-      // flips bit 0) and one coalesced 16-B store -- each warp instruction writes 512 contiguous bytes
+        for (int j = 0; j < 64; j += 2) {
+          const uint32_t chunk = (((uint32_t)j & 15u) >> 1) ^ (t & 7u);
+          *reinterpret_cast<double2*>(xb + 1024u * (uint32_t)(j >> 4) + 16u * t + 2u * chunk) = make_double2(v[j], v[j + 1]);
+        }
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // generic writes -> TMA reads
+        bar.sync();
+        if (t == 0) {
+          const int row = (int)(((uint64_t)(2 * k + p) << H) + yh);
+#pragma unroll
+          for (int b = 0; b < 4; ++b) tma_store_3d(&tmw, 16 * b, 0, row, xb + 1024 * b);
+          asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 64; ++j) xb[xsw12(64u * t + j)] = v[j];
+        bar.sync();
+        // chunk C = t + 64 i holds positions 2C, 2C + 1: one 16-B load (halves swapped when the XOR key
+        // flips bit 0) and one coalesced 16-B store -- each warp instruction writes 512 contiguous bytes
 #pragma unroll 8
-      for (int i = 0; i < 32; ++i) {
-        const uint32_t e = 2u * (t + 64u * i);
-        const uint32_t key = (e >> 6) & 15u;
-        const double2 x = *reinterpret_cast<const double2*>(xb + ((e ^ key) & ~1u));
-        const double2 y = (key & 1u) ? make_double2(x.y, x.x) : x;
-        if (PAW_CS) __stcs(reinterpret_cast<double2*>(wp + e), y);
-        else __stcg(reinterpret_cast<double2*>(wp + e), y);
+        for (int i = 0; i < 32; ++i) {
+          const uint32_t e = 2u * (t + 64u * i);
+          const uint32_t key = (e >> 6) & 15u;
+          const double2 x = *reinterpret_cast<const double2*>(xb + ((e ^ key) & ~1u));
+          const double2 y = (key & 1u) ? make_double2(x.y, x.x) : x;
+          __stcg(reinterpret_cast<double2*>(wp + e), y);
+        }
       }
     };
-    transform_store(wrow);                               // plane A
+    transform_store(wrow, 0);                            // plane A
 #pragma unroll
     for (int c = 0; c < 8; ++c) {                        // plane B back from TMEM
       uint32_t r32[16];
@@ -1343,8 +1371,10 @@ __global__ void __launch_bounds__(256, 1) k_passAw(const double2* __restrict__ p
 #pragma unroll
       for (int i = 0; i < 8; ++i) v[8 * c + i] = __hiloint2double(r32[2 * i + 1], r32[2 * i]);
     }
-    transform_store(wrow + PLANE);                       // plane B
+    transform_store(wrow + PLANE, 1);                    // plane B
   }
+  if constexpr (TS)
+    if (t == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
   tmem_fence_before();
   __syncthreads();
   if (w == 0) tmem_dealloc(tmem_s, 256);

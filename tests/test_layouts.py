@@ -128,3 +128,28 @@ def test_mixed_81_tile_fiber_orders():
     sys.path.insert(0, os.path.join(root, "tools"))
     from mana_tile_order import leg_cost
     assert sum(leg_cost(J, orders[J]) for J in range(4)) == 6768
+
+
+def test_passaw_tma_store_staging():
+    """k_passAw<TS>: after round 1 thread t holds v[j] = position 64 t + j of the row-plane.  It writes
+    the pair (v[j], v[j+1]) as the 16-B chunk at byte 8192 (j >> 4) + 128 t + 16 (((j & 15) >> 1) ^ (t & 7)).
+    The TMA tensor store (box {16 doubles, 64 rows}, SWIZZLE_128B: 16-B chunk bits [4:6] ^= bits [7:9]
+    of the box offset) must read position 64 t + 16 b + jj there, and each quarter-warp STS.128 must hit
+    8 distinct 16-B bank groups."""
+    def tma_image(b, row, jj):                  # where the TMA engine expects box b's element (jj, row)
+        off = 128 * row + 8 * jj
+        return 8192 * b + (off ^ (((off >> 7) & 7) << 4))
+
+    seen = set()
+    for t in range(64):
+        for j in range(0, 64, 2):
+            addr = 8192 * (j >> 4) + 128 * t + 16 * ((((j & 15) >> 1)) ^ (t & 7))
+            assert addr == tma_image(j >> 4, t, j & 15)
+            assert addr + 8 == tma_image(j >> 4, t, (j & 15) + 1)
+            seen.add(addr)
+    assert len(seen) == 64 * 32
+    for j in range(0, 64, 2):
+        for q in range(0, 64, 8):
+            groups = {((8192 * (j >> 4) + 128 * t + 16 * ((((j & 15) >> 1)) ^ (t & 7))) // 16) % 8
+                      for t in range(q, q + 8)}
+            assert len(groups) == 8
