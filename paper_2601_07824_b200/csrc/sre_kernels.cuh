@@ -255,9 +255,10 @@ __device__ __forceinline__ float exp_fast(float z) { return expf(z); }
 // Epilogue of one tile's values per thread into a fresh local sum, then one add into the long-lived
 // accumulators: keeps the running-sum chains short (DESIGN "Summation").  The general-alpha body is
 // compact (ln_fast ~30 SASS instead of the ~120 of log(), which made a full unroll I-cache bound in
-// round 1).  Terms with t below 1e-300 add 0 (t ln t > -1e-297).
+// round 1).  Terms with t below 1e-300 add 0 (t ln t > -1e-297); in FP32 mode the cut is t > 0.
 template <bool A2, class R, int M>
 __device__ __forceinline__ void tile_accumulate(double (&acc)[NACC], const R (&v)[M], const Alphas& al) {
+  constexpr R kTiny = std::is_same<R, double>::value ? R(1e-300) : R(0);
   R loc[NACC];          // FP32 mode: local sums in FP32, one conversion per tile
 #pragma unroll
   for (int i = 0; i < NACC; ++i) loc[i] = R(0);
@@ -302,7 +303,7 @@ __device__ __forceinline__ void tile_accumulate(double (&acc)[NACC], const R (&v
 #pragma unroll
       for (int j = 0; j < M; ++j) {
         const R t = v[j] * v[j];
-        const R x = t > R(1e-300) ? t * ln_tab(t) : R(0);
+        const R x = t > kTiny ? t * ln_tab(t) : R(0);
         if (j & 1) l1 += x; else l0 += x;
       }
       loc[MAXA + 1] += l0 + l1;
@@ -317,7 +318,7 @@ __device__ __forceinline__ void tile_accumulate(double (&acc)[NACC], const R (&v
     for (int j = 0; j < M; ++j) {
       const R t = tv[j];
       loc[MAXA] += t;
-      const bool pos = t > R(1e-300);
+      const bool pos = t > kTiny;
       const R lt = ln_fast(pos ? t : R(1));
       if (al.need_log) loc[MAXA + 1] = fma(t, pos ? lt : R(0), loc[MAXA + 1]);
 #pragma unroll
