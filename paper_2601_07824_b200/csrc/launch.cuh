@@ -120,6 +120,20 @@ cudaError_t launch_mid_t(const typename Cx<V>::T* psi, int N, int B, int gx, uin
                          double* partial, double* chi, cudaStream_t st, const uint64_t* alist,
                            unsigned long long* hist = nullptr) {
   static uint64_t init_mask = 0;   // per device: the attribute belongs to the device context
+  if constexpr (T == 13 && !DBG) {  // N = 14 sweeps: ring-fed generation (k_midr) unless SRE_MIDR=0
+    static const bool ring = [] { const char* e = getenv("SRE_MIDR"); return !(e && e[0] == '0'); }();
+    if (ring && !alist) {
+      constexpr int smem = 2 * padded(1 << T) * (int)sizeof(double) + MR_NS * 1024 * (int)sizeof(typename Cx<V>::T);
+      static uint64_t init_mask_r = 0;
+      cudaError_t e = set_smem_once(k_midr<T, A2, V>, smem, init_mask_r);
+      if (e != cudaSuccess) return e;
+      dim3 grid(gx, B);
+      return launch_counted(LK_SINGLE, st, [&] {
+        k_midr<T, A2, V><<<grid, 256, smem, st>>>(psi, N, a0, count, al, partial, hist);
+        return cudaGetLastError();
+      });
+    }
+  }
   {
     cudaError_t e = set_smem_once(k_mid<T, A2, DBG, V>, SMEM_128K, init_mask);
     if (e != cudaSuccess) return e;

@@ -754,6 +754,102 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(b)) : "memory");
 }
 
+// k_midr: k_mid for T = 13 (N = 14; one 256-thread unit per CTA) with the generation fed by a
+// bulk-copy ring instead of L1/L2 gathers (k_mid is latency-bound on them: long_scoreboard).  For
+// a >= 512 the pivot p >= 9, so the 512 positions y of stage s map to the contiguous x block
+// ins0(512 s, p) + [0, 512), and x ^ a to the block (x_0 ^ (a & ~511)) + (i ^ (a & 511)): one
+// 2 x 512-complex stage per 512 positions, 16 stages per X-string, in an MR_NS-deep ring refilled
+// by the last of the 8 warps to leave a slot.  Thread t takes positions t + 256 e (e = 0, 1) of each
+// stage, i.e. k_mid's register j = 2 s + e.  The CTA's X-strings with a < 512 (a prefix, since a
+// grows with the item index) keep k_mid's global-load generation.
+constexpr int MR_NS = 4;
+template <int T, bool A2, class V = double>
+__global__ void __launch_bounds__(256, 1) k_midr(const typename Cx<V>::T* __restrict__ psi_all, int N, uint64_t a0,
+                                                 uint64_t count, Alphas al, double* partial, unsigned long long* hist) {
+  static_assert(T == 13, "k_midr: one 256-thread unit per CTA");
+  using C2 = typename Cx<V>::T;
+  ln_table_init(!A2 && al.need_log && std::is_same<V, double>::value);   // t ln t pass (tile_accumulate)
+  __shared__ unsigned long long shist[SPEC_BINS];
+  __shared__ __align__(8) uint64_t full[MR_NS];
+  __shared__ int used[MR_NS];
+  if (hist)
+    for (int i = threadIdx.x; i < SPEC_BINS; i += blockDim.x) shist[i] = 0ull;
+  constexpr int SPI = (1 << T) / 512;                                  // stages per X-string
+  extern __shared__ __align__(128) double smem[];
+  V* sm = reinterpret_cast<V*>(smem);
+  C2* ring = reinterpret_cast<C2*>(smem + 2 * padded(1 << T));        // [NS][q 512 | r 512]
+  const typename Cx<V>::T* psi = psi_all + ((size_t)blockIdx.y << N);
+  const uint32_t t = threadIdx.x, lane = t & 31;
+  const uint64_t gx = gridDim.x;
+  const uint64_t my_items = count > blockIdx.x ? (count - 1 - blockIdx.x) / gx + 1 : 0;
+  const uint64_t first = a0 + blockIdx.x;                             // a of item n = first + n gx
+  const uint64_t n0 = first >= 512 ? 0 : (512 - first + gx - 1) / gx;
+  const uint64_t stages = my_items > n0 ? (my_items - n0) * SPI : 0;
+  auto produce = [&](uint64_t s, int slot) {                          // one thread
+    const uint64_t a = first + (n0 + s / SPI) * gx;
+    const int p = 63 - __clzll((long long)a);
+    const uint64_t x0 = ins0(512 * (s % SPI), p);
+    C2* dst = ring + (size_t)slot * 1024;
+    mbar_expect_tx(&full[slot], 2 * 512 * sizeof(C2));
+    bulk_g2s(dst, psi + x0, 512 * sizeof(C2), &full[slot]);
+    bulk_g2s(dst + 512, psi + (x0 ^ (a & ~511ull)), 512 * sizeof(C2), &full[slot]);
+  };
+  if (t == 0) {
+    for (int i = 0; i < MR_NS; ++i) { mbar_init(&full[i], 1); used[i] = 0; }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    for (int i = 0; i < MR_NS; ++i)
+      if ((uint64_t)i < stages) produce(i, i);
+  }
+  __syncthreads();
+  double acc[NACC];
+#pragma unroll
+  for (int i = 0; i < NACC; ++i) acc[i] = 0.0;
+  uint64_t s = 0;
+  for (uint64_t n = 0; n < my_items; ++n) {
+    const uint64_t a = first + n * gx;
+    const int p = pivot_of(a, N);
+    V v[2][32];
+    if (n < n0) {
+      unit_gen<T, V>(psi, 0, a, p, N, t, v);
+    } else {
+      const uint32_t alo = (uint32_t)(a & 511u);
+#pragma unroll
+      for (int c = 0; c < SPI; ++c, ++s) {
+        const int slot = (int)(s % MR_NS);
+        mbar_wait(&full[slot], (uint32_t)(s / MR_NS) & 1u);
+        const C2* cq = ring + (size_t)slot * 1024;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const uint32_t i = t + 256u * e;
+          const C2 q = cq[i];
+          const C2 r = cq[512 + (i ^ alo)];
+          v[0][2 * c + e] = fma(r.x, q.x, r.y * q.y);                  // Re conj(psi_{x^a}) psi_x
+          v[1][2 * c + e] = fma(r.x, q.y, -(r.y * q.x));               // Im
+        }
+        __syncwarp();
+        if (lane == 0 && atomicAdd(&used[slot], 1) == 7) {             // the last warp refills the slot
+          atomicExch(&used[slot], 0);
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          if (s + MR_NS < stages) produce(s + MR_NS, slot);
+        }
+      }
+    }
+    Rounds<T, 0, 0, 2, BarNamed, false, V>::run(v, sm, t, BarNamed{1, 256});
+    tile_accumulate<A2>(acc, v[0], al);
+    tile_accumulate<A2>(acc, v[1], al);
+    if (hist) {
+      spec_add(shist, v[0]);
+      spec_add(shist, v[1]);
+    }
+  }
+  block_flush(acc, partial, blockIdx.y * gridDim.x + blockIdx.x);
+  if (hist) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < SPEC_BINS; i += blockDim.x)
+      if (shist[i]) atomicAdd(hist + i, shist[i]);
+  }
+}
+
 // ------------------------------------------------------------------------------------------
 // Tensor memory (TMEM) as a per-thread register extension.  Thread lane of warp w owns TMEM
 // lane 32 (w % 4) + lane; a double occupies two consecutive 32-bit columns.  tcgen05.ld/st
@@ -882,7 +978,8 @@ constexpr int PA10_SMEM = PA10_NS * 2 * 1024 * 16 + 8 * padded(1024) * 8;  // 12
 // finish with a ring slot refills it with the item NS positions ahead.  Warp w generates
 // X-string 8g + w from the staged rows, transforms 10 bits (one warp-local exchange per
 // plane) and writes its row of both planes.
-template <int N, class V = double, bool ROWM = false>   // ROWM: row-major planes [2^H][1024] (FP64, k_passBw)
+// ROWM: row-major planes [2^H][1024] (FP64, k_passBw)
+template <int N, class V = double, bool ROWM = false>
 __global__ void __launch_bounds__(256, 1) k_passA10s(const typename Cx<V>::T* __restrict__ psi, uint64_t a_first,
                                                      int kcount, int groups, V* __restrict__ ws) {
   using C2 = typename Cx<V>::T;
