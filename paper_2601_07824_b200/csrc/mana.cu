@@ -31,6 +31,7 @@
 
 #include "../../include/sre.h"
 #include "launch.cuh"
+#include "mana_remap_tab.h"
 
 namespace sre_host {
 int fail(int code, const char* fmt, ...);
@@ -340,6 +341,7 @@ struct RowSArgs {
   int H;                // high digits
   int S;                // columns per workspace block
   int PP;               // pairs per item
+  int remap;            // L - G = 5: per-shift lane remap (kManaRemap) of the thread groups
 };
 
 // Digit-shift tables of one X-string's low digits: for ternary digit j of an index k,
@@ -407,15 +409,22 @@ __global__ void __launch_bounds__(kThreads) k_mana_rowS(RowSArgs A) {
   const int nchunk = (A.npairs + A.PP - 1) / A.PP;
   const long items = (long)nh * nchunk;
   const int t = threadIdx.x;
+  // Lane remap (L - G = 5, 243 groups): thread t takes group g = kManaRemap[c][t] for the shift c
+  // = a_l1 / 3^G of each pair, so that each quarter-warp's two 9-block loads (blocks shift(g, c),
+  // neg(g, c)) and its tile store (9 g + i) hit distinct 16-B bank groups (tools/mana_remap_gen.c,
+  // DESIGN.md section 17).  Without it g = t.
+  constexpr bool RMP = (L - G == 5) && (G == 2);
   int td[L - G > 0 ? L - G : 1];     // ternary digits of this thread's group index
-  {
-    int x = t;
+  auto set_group = [&](int g) {
+    int x = g;
 #pragma unroll
     for (int j = 0; j < L - G; ++j) {
       td[j] = x % 3;
       x /= 3;
     }
-  }
+  };
+  set_group(t);
+  int grp = t;
   for (long it = blockIdx.x; it < items; it += gridDim.x) {
     const int h = (int)(it / nchunk), ch = (int)(it % nchunk);
     const int p_lo = ch * A.PP, p_hi = min(A.npairs, p_lo + A.PP);
@@ -444,7 +453,13 @@ __global__ void __launch_bounds__(kThreads) k_mana_rowS(RowSArgs A) {
       int g2s = 0, g2n = 0;                   // rows for a2 when it crosses an a_hi boundary
       if (two && !staged2) tshift_rt(h, ah2, A.H, g2s, g2n);
       if (t < NT) {
-        // upper digits: (t - a_up) and (-t - a_up) digit-wise, from the precomputed digits of t
+        if constexpr (RMP) {
+          if (A.remap) {
+            grp = kManaRemap[al1 / RG][t];
+            set_group(grp);
+          }
+        }
+        // upper digits: (g - a_up) and (-g - a_up) digit-wise, from the digits of the group g
         int us1 = 0, un1 = 0, us2 = 0, un2 = 0;
         {
           int b1 = al1 / RG, b2 = al2 / RG;
@@ -519,7 +534,7 @@ __global__ void __launch_bounds__(kThreads) k_mana_rowS(RowSArgs A) {
         }
         reg_f3<G>(r);
 #pragma unroll
-        for (int i = 0; i < RG; ++i) tile[t * RG + i] = r[i];
+        for (int i = 0; i < RG; ++i) tile[grp * RG + i] = r[i];
       }
       __syncthreads();
       double2* dst = A.ws + (size_t)pl * ((size_t)NBLK * nh * S) + (size_t)h * S;
@@ -869,7 +884,8 @@ int run_mana(const double2* psi, int N, uint64_t a_begin, uint64_t a_end, char* 
         const int PP = std::min(m.PP, np);
         const int gA = grid_for((long)p3(m.H) * ((np + PP - 1) / PP), occA, d.sms);
         const int gB = grid_for((long)np * nblk, occB, d.sms);
-        mana::RowSArgs A{psi, rows, a_begin, a_end, p0, np, m.H, m.S, PP};
+        static const int remap = [] { const char* e = std::getenv("SRE_MANA_REMAP"); return (e && e[0] == '0') ? 0 : 1; }();
+        mana::RowSArgs A{psi, rows, a_begin, a_end, p0, np, m.H, m.S, PP, remap};
         mana::ColCArgs B{rows, slots, np, m.L};
         MCK(launch_counted(LK_PASSA, st, [&] { fa<<<gA, kThreads, m.row_smem, st>>>(A); return cudaGetLastError(); }));
         MCK(launch_counted(LK_PASSB, st, [&] { fb<<<gB, kThreads, smemB, st>>>(B); return cudaGetLastError(); }));

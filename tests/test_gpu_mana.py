@@ -6,6 +6,7 @@ Tolerance: both sums are sums of 9^N non-negative (S_abs) or signed (S_sum) term
 <= 1, each an FP64 transform output with relative error <= N * 4 eps (radix-3 butterflies); the
 sums are compared at rtol 1e-11."""
 import math
+import os
 
 import numpy as np
 import pytest
@@ -81,6 +82,30 @@ def test_strange_product(qm, n):
     import sre_inputs.qutrit as q
     m, _ = qm.mana(_cuda(q.kron([q.strange()] * n)))
     assert m == pytest.approx(n * math.log2(5.0 / 3.0), abs=1e-11)
+
+
+def test_lane_remap_bitwise_and_every_shift_vs_oracle(qm, monkeypatch):
+    """k_mana_rowS<7, 2, S> lane remap (kManaRemap): thread t computes group g = pi_c(t) but stores it
+    at the same tile positions 9 g + i, so the partial sums are bitwise those of the identity order
+    (SRE_MANA_REMAP=0, read at the first call of a process -- hence a subprocess for the reference).
+    The range [4, 2200) covers every shift c = (a_l / 9) mod 243 and is checked against the oracle."""
+    import subprocess
+    import sys
+    from oracle import mana as om
+    import sre_inputs.qutrit as q
+    n, a0, a1 = 12, 4, 2200
+    psi = q.haar(n, 612)
+    got = qm.partial_sums(_cuda(psi), a0, a1).cpu().numpy()
+    np.testing.assert_allclose(got, om.sums_fwht(psi, (a0, a1)), rtol=RTOL)
+    code = ("import numpy as np, torch, sre_inputs.qutrit as q; from paper_2601_07824_b200 import qutrit as qm; "
+            f"psi = torch.from_numpy(q.haar({n}, 612)).cuda(); "
+            f"print(repr(qm.partial_sums(psi, {a0}, {a1}).cpu().numpy().tolist()))")
+    env = dict(os.environ, SRE_MANA_REMAP="0")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    ref = np.array(eval(out.stdout.strip().splitlines()[-1]))
+    assert np.array_equal(got, ref)
 
 
 def test_additivity_and_clifford_n12(qm):

@@ -153,3 +153,35 @@ def test_passaw_tma_store_staging():
             groups = {((8192 * (j >> 4) + 128 * t + 16 * ((((j & 15) >> 1)) ^ (t & 7))) // 16) % 8
                       for t in range(q, q + 8)}
             assert len(groups) == 8
+
+
+def test_mana_remap_table():
+    """csrc/mana_remap_tab.h (tools/mana_remap_gen.c): for every shift c, kManaRemap[c] is a
+    permutation of the 243 thread groups, and the quarter-warp key collisions of the three
+    bank-group maps (g, shift(g, c), neg(g, c), mod 8) total what the header states."""
+    import os
+    import re
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = open(os.path.join(root, "paper_2601_07824_b200", "csrc", "mana_remap_tab.h")).read()
+    stated = int(re.search(r"collisions: total (\d+)", src).group(1))
+    rows = [[int(x) for x in r.split(",")] for r in re.findall(r"\{([0-9,]+)\}", src)]
+    assert len(rows) == 243
+
+    def shift(g, c, neg):
+        r, p = 0, 1
+        for _ in range(5):
+            gd, cd = g % 3, c % 3
+            g, c = g // 3, c // 3
+            r += ((6 - gd - cd) % 3 if neg else (gd - cd + 3) % 3) * p
+            p *= 3
+        return r
+
+    total = 0
+    for c, row in enumerate(rows):
+        assert sorted(row) == list(range(243))
+        for q in range(0, 243, 8):
+            octet = row[q:q + 8]
+            for f in (lambda g: g, lambda g: shift(g, c, 0), lambda g: shift(g, c, 1)):
+                ks = [f(g) % 8 for g in octet]
+                total += sum(ks.count(k) * (ks.count(k) - 1) // 2 for k in set(ks))
+    assert total == stated
