@@ -108,17 +108,23 @@ void two_pass_params(int T, int& L, int& H, int& CB) {
 constexpr int SMALL_MAX_T = 10;
 constexpr int MID_MAX_T = 13;
 
-// CTAs per state for the single-pass kernels: minimise waves x per-CTA items (uniform cost).
-int pick_gx(uint64_t count, int per_cta, int B, int resident) {
-  uint64_t best = ~0ull;
-  int bg = 1;
+// CTAs per state for the single-pass kernels: minimise waves x per-CTA items (uniform cost).  With
+// slack > 0 the smallest g within (1 + slack) of that minimum: fewer, longer CTAs amortise a per-CTA
+// start (k_midr's ring fill) at no modelled cost.
+int pick_gx(uint64_t count, int per_cta, int B, int resident, double slack = 0.0) {
   const uint64_t maxg = (count + per_cta - 1) / per_cta;
-  for (int g = 1; g <= 4096 && (uint64_t)g <= maxg; ++g) {
+  auto cost = [&](int g) {
     const uint64_t waves = ((uint64_t)B * g + resident - 1) / resident;
     const uint64_t items = (count + (uint64_t)g * per_cta - 1) / ((uint64_t)g * per_cta);
-    const uint64_t cost = waves * items;
-    if (cost < best) { best = cost; bg = g; }
-  }
+    return waves * items;
+  };
+  uint64_t best = ~0ull;
+  int bg = 1;
+  for (int g = 1; g <= 4096 && (uint64_t)g <= maxg; ++g)
+    if (cost(g) < best) { best = cost(g); bg = g; }
+  if (slack > 0.0)
+    for (int g = 1; g < bg; ++g)
+      if ((double)cost(g) <= (double)best * (1.0 + slack)) return g;
   return bg;
 }
 
@@ -273,7 +279,7 @@ int run_range_t(const typename Cx<V>::T* psi, const Plan& p, const Dev& d, int N
         const int G = p.T >= 5 ? 32 : (1 << p.T);
         gx = pick_gx(count, 256 / G, B, occupancy_small(p.T, d));
       } else {
-        gx = pick_gx(count, 256 >> (p.T - 5), B, d.sms);
+        gx = pick_gx(count, 256 >> (p.T - 5), B, d.sms, 0.01);
       }
       if ((size_t)gx > p.slots) gx = (int)p.slots;
       CK(cudaMemsetAsync(partial, 0, sizeof(double) * (size_t)gx * B * NACC, st));
