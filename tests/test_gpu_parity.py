@@ -270,3 +270,32 @@ def test_exact_resumable_matches_exact(sre, tmp_path):
     m, ln = exact_resumable(psi, [2.0], chunk=4096, journal_path=j)
     m0, ln0 = sre.exact(psi, [2.0])
     assert abs(m[0] - m0[0]) < 1e-12 and abs(ln - ln0) < 1e-12
+
+
+def _sums_in_subprocess(env_extra, n, seed, lo, hi, alphas, batch=0):
+    """partial_sums in a fresh process (the kernel-variant switches are read once per process)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    gen = f"si.haar_batch({n}, {batch}, {seed})" if batch else f"si.haar({n}, {seed})"
+    code = ("import numpy as np, torch, sre_inputs as si, paper_2601_07824_b200 as sre; "
+            f"psi = torch.from_numpy({gen}).cuda(); "
+            f"print(repr(sre.partial_sums(psi, {lo}, {hi}, {alphas!r}).cpu().numpy().tolist()))")
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, **env_extra),
+                         capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-2000:]
+    return np.array(eval(out.stdout.strip().splitlines()[-1]))
+
+
+@pytest.mark.parametrize("env,n,lo,hi,batch", [
+    ({"SRE_MIDR": "0"}, 14, 0, 1 << 14, 4),          # k_midr ring-fed generation vs k_mid's L2 gathers
+    ({"SRE_PAW_TMA": "0"}, 22, 4096, 4096 + 256, 0),   # k_passAw TMA-store exit vs coalesced STG exit
+])
+def test_kernel_variants_bitwise(sre, env, n, lo, hi, batch):
+    """The round-2 variants move the same values by other means (bulk-copy ring instead of gathers,
+    TMA tensor store instead of STG); grids and accumulation order are unchanged, so the raw sums
+    are bitwise those of the variant they replace."""
+    alphas = [1.0, 2.0, 3.0]
+    a = _sums_in_subprocess({}, n, 4242, lo, hi, alphas, batch)
+    b = _sums_in_subprocess(env, n, 4242, lo, hi, alphas, batch)
+    assert np.array_equal(a, b)
