@@ -224,6 +224,15 @@ int sre_mana_partial_sums(const void* psi, int N, uint64_t a_begin, uint64_t a_e
  */
 int sre_mana(const void* psi, int N, double* out_mana, double* out_norm2);
 
+/*
+ * sre_mana_finalize -- host-side Eq. (10) (DESIGN C18) from complete sums over
+ * all 3^N X-strings (e.g. sre_mana_partial_sums shards added over ranks):
+ *   sums_host : HOST double[2] = (S_abs, S_sum).
+ *   out_mana  : log2(S_abs / 3^N).   out_norm2 (may be NULL): S_sum / 3^N = ||psi||^2.
+ * Errors: SRE_EINVAL (NULL, S_abs <= 0), SRE_ERANGE (N).  No device work; needs no GPU.
+ */
+int sre_mana_finalize(const double* sums_host, int N, double* out_mana, double* out_norm2);
+
 /* ============================================================================================
  * Mixed-state qutrit mana (NEXT-4): Algorithm 6, Sec. 3.4 (Eq. (45)).
  *

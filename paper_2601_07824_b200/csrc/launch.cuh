@@ -1,5 +1,5 @@
 // launch.cuh -- host-side launch templates shared by the kernel-family translation units.
-// Each family .cu file (k_small.cu, k_mid.cu, k_generic.cu, k_stageA.cu, k_stageB.cu, k_exp.cu)
+// Each family .cu file (k_small.cu, k_mid.cu, k_generic.cu, k_stageA.cu, k_stageB.cu)
 // explicitly instantiates its dispatchers; sre_api.cu sees them as extern templates, so the
 // kernels compile once each and in parallel (paper_2601_07824_b200/_build.py).
 #pragma once

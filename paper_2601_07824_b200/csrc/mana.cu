@@ -975,6 +975,16 @@ int sre_mana_partial_sums(const void* psi, int N, uint64_t a_begin, uint64_t a_e
                   ws_bytes, sums_dev, reinterpret_cast<cudaStream_t>(stream));
 }
 
+int sre_mana_finalize(const double* sums_host, int N, double* out_mana, double* out_norm2) {
+  if (!sums_host || !out_mana) return fail(SRE_EINVAL, "NULL argument");
+  if (N < 1 || N > SRE_MANA_MAX_N) return fail(SRE_ERANGE, "N=%d outside [1, %d]", N, SRE_MANA_MAX_N);
+  const double D = std::pow(3.0, N);                      // exact for N <= 16 (3^16 < 2^53)
+  if (!(sums_host[0] > 0.0)) return fail(SRE_EINVAL, "S_abs = %.17g is not positive", sums_host[0]);
+  *out_mana = std::log2(sums_host[0] / D);                // Eq. (10): log2(sum_u |W_u|) = log2(S_abs / 3^N)
+  if (out_norm2) *out_norm2 = sums_host[1] / D;           // S_sum = 3^N ||psi||^2
+  return SRE_OK;
+}
+
 int sre_mana(const void* psi, int N, double* out_mana, double* out_norm2) {
   if (!psi) return fail(SRE_EINVAL, "psi is NULL");
   if (N < 1 || N > SRE_MANA_MAX_N) return fail(SRE_ERANGE, "N=%d outside [1, %d]", N, SRE_MANA_MAX_N);

@@ -99,13 +99,13 @@ def shard_bounds(total: int, rank: int, world: int):
 
 def mana_sharded(n: int, rank: int, world: int, partial_fn: Callable, allreduce_fn: Callable):
     """partial_fn(lo, hi) -> [2] sums over X-strings [lo, hi) of 3^n; allreduce_fn sums them in
-    place over ranks.  Returns (mana = log2(sum|chi| / 3^n), ||psi||^2 = sum chi / 3^n)."""
-    import math
+    place over ranks.  Returns (mana = log2(sum|chi| / 3^n), ||psi||^2 = sum chi / 3^n) from the
+    library's host-side sre_mana_finalize (Eq. (10))."""
+    from .qutrit import finalize
     lo, hi = shard_bounds(3 ** n, rank, world)
     sums = partial_fn(lo, hi)
     allreduce_fn(sums)
-    s = [float(x) for x in sums.cpu().reshape(-1)] if hasattr(sums, "cpu") else [float(x) for x in sums]
-    return math.log2(s[0] / 3 ** n), s[1] / 3 ** n
+    return finalize(sums, n)
 
 
 def mana(psi, group=None, workspace=None):

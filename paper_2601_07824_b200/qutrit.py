@@ -30,6 +30,8 @@ def _lib():
         lib.sre_mana_partial_sums.restype = i
         lib.sre_mana.argtypes = [vp, i, dp, dp]
         lib.sre_mana.restype = i
+        lib.sre_mana_finalize.argtypes = [dp, i, dp, dp]
+        lib.sre_mana_finalize.restype = i
         lib.sre_mana_mixed_workspace_size.argtypes = [i]
         lib.sre_mana_mixed_workspace_size.restype = ctypes.c_size_t
         lib.sre_mana_mixed_sums.argtypes = [vp, i, vp, ctypes.c_size_t, vp, vp]
@@ -78,6 +80,18 @@ def mana(psi):
     n2 = ctypes.c_double(0.0)
     _check(lib.sre_mana(ctypes.c_void_p(ptr), n, ctypes.byref(m), ctypes.byref(n2)))
     del keep
+    return m.value, n2.value
+
+
+def finalize(sums, n: int):
+    """(mana, ||psi||^2) from complete sums (S_abs, S_sum) over all 3^n X-strings, through the
+    library's host-side sre_mana_finalize (Eq. (10); no GPU needed)."""
+    import numpy as np
+    s = np.ascontiguousarray(np.asarray(sums.cpu() if hasattr(sums, "cpu") else sums, dtype=np.float64).reshape(-1)[:2])
+    lib = _lib()
+    m, n2 = ctypes.c_double(), ctypes.c_double()
+    _check(lib.sre_mana_finalize(s.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), int(n), ctypes.byref(m),
+                                 ctypes.byref(n2)))
     return m.value, n2.value
 
 

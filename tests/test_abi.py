@@ -72,3 +72,17 @@ def test_finalize_matches_oracle(lib, oracle_lib):
         assert abs(ln_lib[0] - ln_or) < 1e-16
     m, ln = sre.finalize(np.array([2.0 ** 16, 2.0 ** 16, 0.0]), 16, [2.0])
     assert m[0, 0] == 0.0 and math.copysign(1.0, m[0, 0]) == -1.0 and ln[0] == 0.0
+
+
+def test_mana_finalize_host(lib):
+    """sre_mana_finalize (host-side Eq. (10), no GPU): mana = log2(S_abs / 3^N), ||psi||^2 = S_sum / 3^N;
+    the strange state's sum |W| = 5/3 per qutrit (DESIGN section 15 pins) gives N log2(5/3)."""
+    from paper_2601_07824_b200 import SreError, qutrit
+    for n in (1, 4, 12):
+        m, n2 = qutrit.finalize([3.0 ** n * (5.0 / 3.0) ** n, 3.0 ** n], n)
+        assert abs(m - n * math.log2(5.0 / 3.0)) < 1e-13 and abs(n2 - 1.0) < 1e-15
+    m, n2 = qutrit.finalize(np.array([3.0 ** 10, 3.0 ** 10 * 0.5]), 10)   # stabilizer: mana 0
+    assert m == 0.0 and n2 == 0.5
+    for bad in (([0.0, 1.0], 3), ([1.0, 1.0], 0), ([1.0, 1.0], 17)):
+        with pytest.raises(SreError):
+            qutrit.finalize(*bad)
