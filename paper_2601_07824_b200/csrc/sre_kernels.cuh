@@ -968,7 +968,7 @@ __device__ __forceinline__ void transform10_tmem(uint32_t tm, double (&v)[2][32]
   bfly_bit<4>(v[0]); bfly_bit<4>(v[1]);                   // e0
 }
 
-constexpr int PA10_NS = 4;                                   // staging ring depth
+constexpr int PA10_NS = 4;                                   // staging ring depth (6 measured no better at N = 20)
 constexpr int PA10_SMEM = PA10_NS * 2 * 1024 * 16 + 8 * padded(1024) * 8;  // 128 KB ring + 66 KB exchange
 
 // Staged pass A for L = 10 (N = 15..20).  A persistent CTA of 8 warps walks items
@@ -1322,8 +1322,8 @@ __device__ __forceinline__ uint32_t xsw13(uint32_t e) { return e ^ (((e >> 7) & 
 // quarter-warp), and the TMA engine reads the 32 KB back from shared memory and writes whole 128-B
 // lines -- no LDS/STG wavefronts on the L1TEX pipe.  !TS: natural-order staging in the XOR-swizzled
 // buffer and coalesced 16-B stores (A/B measurements, SRE_PAW_TMA=0).
-constexpr int PAW_NS = 4;                                             // ring stages (16 KB each)
-constexpr int PAW_SMEM = PAW_NS * 2 * 512 * 16 + 4 * 4096 * 8 + 1024; // 64 KB ring + 4 x 32 KB buffers + alignment
+constexpr int PAW_NS = 6;                                             // ring stages (16 KB each)
+constexpr int PAW_SMEM = PAW_NS * 2 * 512 * 16 + 4 * 4096 * 8 + 1024; // 96 KB ring + 4 x 32 KB buffers + alignment
 
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* tmap, int c0, int c1, int c2, const void* src) {
   asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n"
